@@ -1,0 +1,168 @@
+/*
+ * leann_b200.h — C-ABI of the B200-native LEANN search hot path.
+ *
+ * This is the drop-in boundary for the reference's query path. The reference
+ * (slimvec 0.1.0, pure Python) has no FFI; its boundaries are Python duck
+ * types, and each entry point below replaces one of them:
+ *
+ *   lv_index_create      <- Engine.open loaders: load_graph (graph.py:151-193),
+ *                           load_pq (pq.py:213-244), load_deleted (graph.py:204-216)
+ *   lv_index_set_matrix  <- MatrixSource(matrix) oracle source (search.py:78-93)
+ *   lv_index_set_cache   <- build_embedding_cache / EmbeddingCache (search.py:113-142)
+ *   lv_index_attach_encoder
+ *                        <- ProviderSource(provider, store.get) (search.py:96-110)
+ *                           + provider.embed_batch (vectors.py:201-211)
+ *   lv_search_batch      <- run_search(graph, q, params, source, metric, pq_model,
+ *                           pq_codes, cache) (search.py:434-443), batched over B queries:
+ *                           two_level_search (search.py:331-431) and
+ *                           best_first_search (search.py:288-328)
+ *   lv_adc_tables        <- adc_build (pq.py:153-178)
+ *   lv_adc_score         <- approx_distance_many (pq.py:186-189)
+ *   lv_distance_many     <- distance_many (vectors.py:120-140)
+ *   lv_encoder_create / lv_encode
+ *                        <- provider.embed_batch for token payloads (vectors.py:201-211)
+ *
+ * Conventions: plain pointers and sizes only. Unless LV_IO_DEVICE is set in a
+ * call's flags, array arguments are HOST pointers and the call copies them
+ * through pinned staging on `stream` and synchronises before returning.
+ * With LV_IO_DEVICE they are device pointers and the call is stream-ordered.
+ * Return codes map onto the reference's SlimvecError.code (errors.py:11-93):
+ * usage -> LV_ERR_USAGE, data -> LV_ERR_DATA, provider -> LV_ERR_PROVIDER,
+ * internal -> LV_ERR_INTERNAL (same numbers as the CLI exit codes, cli.py:16).
+ * A handle is used by one host thread at a time; one handle per GPU/rank.
+ */
+#ifndef LEANN_B200_H
+#define LEANN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LV_OK 0
+#define LV_ERR_USAGE 2
+#define LV_ERR_DATA 3
+#define LV_ERR_PROVIDER 4
+#define LV_ERR_INTERNAL 5
+
+/* metric tags: the LPQ1 header byte order (pq.py:193-195, vectors.py:19) */
+#define LV_METRIC_L2 0
+#define LV_METRIC_IP 1
+#define LV_METRIC_COSINE 2
+
+/* search modes (search.py:32) */
+#define LV_MODE_EXACT_BESTFIRST 0
+#define LV_MODE_TWO_LEVEL 1
+
+/* exact-vector sources */
+#define LV_SOURCE_MATRIX 0   /* resident matrix (MatrixSource) */
+#define LV_SOURCE_ENCODER 1  /* recompute with the attached encoder (ProviderSource) */
+
+#define LV_IO_DEVICE 1       /* pointer arguments are device pointers */
+
+/* per-query status codes written to lv_search_outputs.status */
+#define LV_Q_OK 0
+#define LV_Q_AQ_OVERFLOW 1   /* retried internally with a larger queue; never returned */
+#define LV_Q_FAILED 2
+
+typedef struct lv_index lv_index;
+typedef struct lv_encoder lv_encoder;
+
+/* One loaded index (LGR1 graph + LPQ1 PQ + LDL1 deletes), host arrays. */
+typedef struct {
+  int64_t n;                                /* nodes */
+  int32_t dim;                              /* embedding dim */
+  int32_t metric;                           /* LV_METRIC_* */
+  int32_t max_degree;                       /* LGR1 M (caps every CSR row) */
+  int32_t level_count;                      /* >= 1 */
+  int64_t entry_point;
+  const uint64_t *const *level_offsets;     /* [level_count] x u64[n+1] */
+  const uint32_t *const *level_neighbors;   /* [level_count] x u32[nnz_l] */
+  const uint64_t *level_nnz;                /* [level_count] */
+  const uint8_t *deleted;                   /* u8[n] 0/1, or NULL */
+  int32_t pq_m;                             /* 0 = no PQ (best-first only) */
+  int32_t pq_padded_dim;
+  const float *pq_codebooks;                /* f32[m][256][padded/m] */
+  const uint8_t *pq_codes;                  /* u8[n][m] */
+} lv_index_desc;
+
+typedef struct {
+  int32_t k;
+  int32_t ef;
+  double rerank_percent;   /* (0, 100] */
+  int32_t batch_size;      /* only shapes the host-side batch log */
+  int32_t mode;            /* LV_MODE_* */
+  int32_t source;          /* LV_SOURCE_* */
+  int32_t use_cache;       /* consult the lv_index_set_cache set */
+  int32_t max_inflight;    /* concurrent query slots; 0 = automatic */
+  int32_t flags;           /* LV_IO_DEVICE */
+} lv_search_params;
+
+typedef struct {
+  int64_t *ids;            /* [B*k], -1 padded */
+  float *dist;             /* [B*k] */
+  int32_t *count;          /* [B] results returned (<= k) */
+  int64_t *counters;       /* [B*4]: recomputations, approx_lookups, cache_hits, expansions */
+  int32_t *status;         /* [B] LV_Q_*; may be NULL */
+  int32_t *visits;         /* optional [B*visits_cap]: base-layer expansion order */
+  int32_t visits_cap;
+  int32_t *batch_log;      /* optional [B*batch_log_cap]: per-call recompute sizes */
+  int32_t batch_log_cap;
+} lv_search_outputs;
+
+/* Aggregate statistics of the last lv_search_batch on a handle. */
+typedef struct {
+  int64_t iterations;        /* frontier launches (encoder mode) */
+  int64_t logical_recomputes;
+  int64_t physical_encodes;  /* passages run through the encoder */
+  double frontier_ms;        /* device time in frontier kernels */
+  double encoder_ms;         /* device time in the encoder */
+  double total_ms;
+  int64_t adc_bytes;         /* algorithmic bytes of ADC+gather */
+} lv_search_stats;
+
+typedef struct {
+  int32_t arch;         /* 0 = BERT-style post-LN GELU, mean pool (C1-C3) */
+  int32_t layers;
+  int32_t hidden;
+  int32_t heads;
+  int32_t ffn;
+  int32_t vocab;
+  int32_t max_seq;
+  int32_t precision;    /* 0 = fp32 (parity mode), 1 = bf16 tcgen05 */
+} lv_encoder_config;
+
+const char *lv_last_error(void);
+int lv_version(void);
+
+int lv_index_create(const lv_index_desc *desc, int device, lv_index **out);
+void lv_index_destroy(lv_index *index);
+int lv_index_set_matrix(lv_index *index, const float *matrix, int flags);
+int lv_index_set_deleted(lv_index *index, const uint8_t *deleted, int flags);
+int lv_index_set_cache(lv_index *index, const int64_t *ids, int64_t count, int flags);
+int lv_index_attach_encoder(lv_index *index, lv_encoder *enc, const void *tokens,
+                            int32_t token_bytes, int32_t seq_len, int flags);
+
+int lv_search_batch(lv_index *index, const float *q, const float *qnorm, int32_t B,
+                    const lv_search_params *params, const lv_search_outputs *out,
+                    void *stream);
+int lv_last_search_stats(const lv_index *index, lv_search_stats *stats);
+
+int lv_adc_tables(lv_index *index, const float *q, const float *qnorm, int32_t B,
+                  float *tables, int flags, void *stream);
+int lv_adc_score(lv_index *index, const float *table, const int64_t *ids, int64_t count,
+                 float *out, int flags, void *stream);
+int lv_distance_many(int32_t metric, const float *rows, int64_t nrows, int32_t dim,
+                     const float *q, float qnorm, float *out, int flags, void *stream);
+
+int lv_encoder_create(const lv_encoder_config *cfg, const float *const *weights,
+                      int32_t n_weights, int device, lv_encoder **out);
+void lv_encoder_destroy(lv_encoder *enc);
+int lv_encode(lv_encoder *enc, const void *tokens, int32_t token_bytes, int64_t n_seqs,
+              int32_t seq_len, float *out, int flags, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEANN_B200_H */

@@ -1,0 +1,113 @@
+// lv_numerics.cuh — bit-exact device restatement of the reference's float math.
+//
+// distance_many (vectors.py:120-140) and adc_build (pq.py:153-178) use
+// np.einsum in float32; approx_distance_many (pq.py:186-189) sums float32 LUT
+// entries in float64 with numpy's pairwise reduction. The orders are pinned
+// in oracle/numerics.py and tests/test_oracle_golden.py; every op below is a
+// separately rounded IEEE op (no FMA contraction: __fmul_rn / __fadd_rn).
+#pragma once
+#include <cstdint>
+
+namespace lv {
+
+// One of the 4 einsum lanes of a length-`dim` dot product: lane `l` sums the
+// elements j+4k+l of each 16-block in the order k = 3,2,1,0, then the
+// zero-padded 4-wide tail. `A`/`B` may be the same pointer (norms).
+template <bool kL2>
+__device__ __forceinline__ float einsum_lane(const float *__restrict__ a,
+                                             const float *__restrict__ b, int dim, int l) {
+  float acc = 0.0f;
+  int j = 0;
+  for (; dim - j >= 16; j += 16) {
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+      float x = a[j + 4 * k + l], y = b[j + 4 * k + l];
+      if (kL2) {
+        float t = __fsub_rn(x, y);
+        acc = __fadd_rn(acc, __fmul_rn(t, t));
+      } else {
+        acc = __fadd_rn(acc, __fmul_rn(x, y));
+      }
+    }
+  }
+  for (; j < dim; j += 4) {
+    float p = 0.0f;
+    if (j + l < dim) {
+      float x = a[j + l], y = b[j + l];
+      if (kL2) {
+        float t = __fsub_rn(x, y);
+        p = __fmul_rn(t, t);
+      } else {
+        p = __fmul_rn(x, y);
+      }
+    }
+    acc = __fadd_rn(acc, p);
+  }
+  return acc;
+}
+
+__device__ __forceinline__ float einsum_combine(float a0, float a1, float a2, float a3) {
+  return __fadd_rn(0.0f, __fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3)));
+}
+
+// Full single-thread einsum dot (all 4 lanes sequentially) — used for short
+// vectors (PQ sub-spaces).
+template <bool kL2>
+__device__ __forceinline__ float einsum_dot_1t(const float *a, const float *b, int dim) {
+  float r0 = einsum_lane<kL2>(a, b, dim, 0);
+  float r1 = einsum_lane<kL2>(a, b, dim, 1);
+  float r2 = einsum_lane<kL2>(a, b, dim, 2);
+  float r3 = einsum_lane<kL2>(a, b, dim, 3);
+  return einsum_combine(r0, r1, r2, r3);
+}
+
+// Final distance from the einsum results (vectors.py:130-139).
+// metric: 0 l2, 1 ip, 2 cosine. For l2 `dot` already holds sum((r-q)^2).
+__device__ __forceinline__ float finish_distance(int metric, float dot, float nrm, float qn) {
+  if (metric == 0) return dot;
+  if (metric == 1) return -dot;
+  float rn = __fsqrt_rn(nrm);
+  return -__fdiv_rn(dot, __fmul_rn(rn, qn));
+}
+
+// numpy pairwise float64 sum of x[0..n) (n <= 128), 8 strided accumulators.
+template <typename Get>
+__device__ __forceinline__ double pairwise_block(Get get, int lo, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, get(lo + i));
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = get(lo + k);
+  int i = 8;
+  int lim = n - (n % 8);
+  for (; i < lim; i += 8) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], get(lo + i + k));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, get(lo + i));
+  return res;
+}
+
+// n <= 256: one level of numpy's recursive split above 128.
+template <typename Get>
+__device__ __forceinline__ double pairwise_sum(Get get, int n) {
+  if (n <= 128) return pairwise_block(get, 0, n);
+  int half = (n / 2) - ((n / 2) % 8);
+  return __dadd_rn(pairwise_block(get, 0, half), pairwise_block(get, half, n - half));
+}
+
+// approx distance of one code row against one LUT (pq.py:186-189).
+__device__ __forceinline__ float adc_one(const float *__restrict__ lut,
+                                         const uint8_t *__restrict__ code, int m) {
+  auto get = [&](int s) -> double {
+    return (double)__ldg(lut + s * 256 + __ldg(code + s));
+  };
+  return __double2float_rn(pairwise_sum(get, m));
+}
+
+}  // namespace lv

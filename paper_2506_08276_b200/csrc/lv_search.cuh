@@ -1,0 +1,106 @@
+// lv_search.cuh — host/device contract of the batched search kernels.
+#pragma once
+#include "lv_common.cuh"
+
+namespace lv {
+
+enum Phase : int32_t { PH_IDLE = 0, PH_ENTRY = 1, PH_DESCENT = 2, PH_BASE = 3, PH_FINISHED = 4 };
+
+constexpr uint32_t kVisited = 0x80000000u;
+constexpr int kWarpsPerBlock = 4;
+
+// Scalar state of one query slot (kept in registers by its warp while running).
+struct SlotState {
+  int32_t qi;        // query index being served, -1 when idle
+  int32_t phase;     // Phase
+  int32_t level;     // current upper level during descent
+  int32_t cur;       // descent position
+  float cur_d;
+  int32_t eq_size;
+  int32_t eq_hint;   // every EQ entry before this index is visited
+  int32_t aq_len;
+  int32_t xl_len;
+  int32_t req_n;     // ids in the pending request
+  int32_t req_off;   // offset of this slot's misses in the global request buffer
+  int32_t n_elig;    // eligible (not yet promoted) AQ entries
+  int32_t status;
+  int32_t visits_n;
+  int32_t blog_n;
+  int32_t pad_;
+  long long recomps;
+  long long approx;
+  long long hits;
+  long long expansions;
+};
+
+struct SearchCtx {
+  // graph (graph.py:30-73)
+  int64_t n;
+  int32_t dim, metric, max_degree, level_count;
+  int32_t entry;
+  const uint64_t *offs[kMaxLevels];
+  const uint32_t *nbrs[kMaxLevels];
+  const uint32_t *deleted_bits;  // may be null
+  const uint32_t *cached_bits;   // may be null (cache off)
+  const int32_t *cache_slot;     // node -> row of cache_rows (encoder source)
+  const float *cache_rows;
+  // PQ (pq.py:40-76)
+  int32_t m;
+  const uint8_t *codes;
+  const float *luts;  // [B][m][256]
+  // exact-vector source
+  int32_t source;
+  const float *matrix;   // [n][dim]  (LV_SOURCE_MATRIX)
+  const float *emb_buf;  // [greq_cap][dim]  (LV_SOURCE_ENCODER)
+  // queries
+  int32_t B;
+  const float *q;   // [B][dim]
+  const float *qn;  // [B]
+  // params (search.py:37-56)
+  int32_t k, ef, mode;
+  double alpha;     // rerank_percent / 100.0, computed on the host in float64
+  // slots
+  int32_t slots, aq_cap, req_cap, xl_cap;
+  int64_t words;    // bitmap words per slot
+  SlotState *st;
+  float *eq_d;
+  uint32_t *eq_id;
+  unsigned long long *aq;
+  uint32_t *abits, *xbits;
+  int32_t *xlist;
+  int32_t *req;
+  // global request buffer (encoder source)
+  int32_t *greq;
+  int32_t *greq_total;
+  int32_t greq_cap;
+  int32_t *queue_head;
+  int32_t *done_count;
+  // outputs
+  int64_t *out_ids;
+  float *out_dist;
+  int32_t *out_count;
+  int64_t *out_counters;
+  int32_t *out_status;
+  int32_t *visits;
+  int32_t visits_cap;
+  int32_t *blog;
+  int32_t blog_cap;
+};
+
+__host__ __device__ inline size_t frontier_smem_per_warp(int max_degree, int req_cap) {
+  size_t per = (size_t)max_degree * 16 + (size_t)req_cap * 8 + (size_t)max_degree * 4;
+  return (per + 15) & ~size_t(15);
+}
+
+// launchers (lv_search.cu)
+cudaError_t launch_lut(const float *q, const float *qn, int B, int dim, int metric,
+                       const float *codebooks, int m, int padded, float *luts, cudaStream_t s);
+cudaError_t launch_adc_score(const float *lut, int m, const uint8_t *codes, const int64_t *ids,
+                             int64_t count, float *out, cudaStream_t s);
+cudaError_t launch_distance_many(int metric, const float *rows, int64_t nrows, int dim,
+                                 const float *q, float qn, float *out, cudaStream_t s);
+cudaError_t launch_slot_reset(SlotState *st, int slots, cudaStream_t s);
+cudaError_t launch_frontier(const SearchCtx &ctx, cudaStream_t s);
+size_t frontier_smem_bytes(const SearchCtx &ctx);
+
+}  // namespace lv

@@ -1,0 +1,105 @@
+"""CPU-side checks of the C-ABI boundary: the library builds, loads and exports
+every entry point declared in include/leann_b200.h (no compute without a GPU)."""
+from __future__ import annotations
+
+import re
+
+import pytest
+
+from conftest import ROOT
+
+
+def _declared():
+    text = (ROOT / "include" / "leann_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(lv_[a-z_]+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for required in ("lv_index_create", "lv_search_batch", "lv_adc_tables", "lv_adc_score",
+                     "lv_distance_many", "lv_encoder_create", "lv_encode", "lv_last_error"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    import __graft_entry__ as ge
+    ge.build()
+    from paper_2506_08276_b200 import _lib
+    lib = _lib.lib()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert lib.lv_version() == 1
+
+
+def test_product_path_fails_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2506_08276_b200 as lv
+    from paper_2506_08276_b200.errors import DeviceError
+    g = lv.load_graph(ROOT / "tests" / "golden" / "small_cos" / "graph.bin")
+    m, c = lv.load_pq(ROOT / "tests" / "golden" / "small_cos" / "pq.bin")
+    with pytest.raises(DeviceError):
+        lv.DeviceIndex(g, m, c)
+
+
+def test_search_params_validation():
+    import paper_2506_08276_b200 as lv
+    from paper_2506_08276_b200.errors import InvalidArgumentError
+    for kw in (dict(k=0), dict(k=5, ef=3), dict(rerank_percent=0.0), dict(batch_size=0),
+               dict(mode="dfs"), dict(cache_percent=101.0)):
+        with pytest.raises(InvalidArgumentError):
+            lv.SearchParams(**kw)
+
+
+def test_formats_round_trip(tmp_path):
+    import numpy as np
+    import paper_2506_08276_b200 as lv
+    from paper_2506_08276_b200.errors import FormatError
+    d = ROOT / "tests" / "golden" / "small_cos"
+    g = lv.load_graph(d / "graph.bin")
+    lv.save_graph(g, tmp_path / "g.bin")
+    assert (tmp_path / "g.bin").read_bytes() == (d / "graph.bin").read_bytes()
+    m, c = lv.load_pq(d / "pq.bin")
+    lv.save_pq(m, c, tmp_path / "p.bin")
+    assert (tmp_path / "p.bin").read_bytes() == (d / "pq.bin").read_bytes()
+    data = (d / "graph.bin").read_bytes()
+    for cut in (3, 10, len(data) - 2):
+        (tmp_path / "t.bin").write_bytes(data[:cut])
+        with pytest.raises(FormatError):
+            lv.load_graph(tmp_path / "t.bin")
+    (tmp_path / "t.bin").write_bytes(data + b"zz")
+    with pytest.raises(FormatError) as err:
+        lv.load_graph(tmp_path / "t.bin")
+    assert "trailing" in str(err.value)
+    bad = bytearray(data)
+    bad[:4] = b"NOPE"
+    (tmp_path / "t.bin").write_bytes(bytes(bad))
+    with pytest.raises(FormatError) as err:
+        lv.load_graph(tmp_path / "t.bin")
+    assert err.value.section == "graph.magic"
+    dl = np.zeros(g.n, bool)
+    dl[::7] = True
+    lv.save_deleted(dl, tmp_path / "d.bin")
+    assert np.array_equal(lv.load_deleted(tmp_path / "d.bin", g.n), dl)
+
+
+def test_validate_catches_violations():
+    import numpy as np
+    import paper_2506_08276_b200 as lv
+    from paper_2506_08276_b200.errors import FormatError
+
+    def mk(rows, max_degree=4):
+        off = np.zeros(len(rows) + 1, np.uint64)
+        flat = []
+        for v, r in enumerate(rows):
+            flat.extend(r)
+            off[v + 1] = len(flat)
+        return lv.PrunedGraph(n=len(rows), max_degree=max_degree, entry_point=0,
+                              levels=np.zeros(len(rows), np.uint16), level_offsets=[off],
+                              level_neighbors=[np.asarray(flat, np.uint32)])
+    lv.validate(mk([[1], [0]]))
+    for rows, md in (([[0], []], 4), ([[1, 1], [], []], 4), ([[1, 2, 3], [], [], []], 2),
+                     ([[7], []], 4)):
+        with pytest.raises(FormatError):
+            lv.validate(mk(rows, md))
