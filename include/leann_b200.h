@@ -20,7 +20,13 @@
  *   lv_adc_score         <- approx_distance_many (pq.py:186-189)
  *   lv_distance_many     <- distance_many (vectors.py:120-140)
  *   lv_encoder_create / lv_encode
- *                        <- provider.embed_batch for token payloads (vectors.py:201-211)
+ *                        <- provider.embed_batch for token payloads (vectors.py:201-211);
+ *                           lv_encoder_profile / lv_encoder_stats replace the reference's
+ *                           SearchReport.stage_times["embed"] instrumentation (search.py:66,
+ *                           :159-187) with device-timed GEMM counters
+ *   lv_gemm_bf16         <- the dense contraction inside embed_batch (no reference
+ *                           counterpart: the reference's provider is a hash, vectors.py:168-189);
+ *                           exported for unit tests of the tcgen05 GEMM
  *
  * Conventions: plain pointers and sizes only. Unless LV_IO_DEVICE is set in a
  * call's flags, array arguments are HOST pointers and the call copies them
@@ -123,6 +129,13 @@ typedef struct {
 } lv_search_stats;
 
 typedef struct {
+  int64_t passages;       /* sequences encoded since the last reset */
+  int64_t gemm_launches;  /* timed GEMM launches (profile mode) */
+  double gemm_ms;         /* summed CUDA-event time of those launches */
+  double gemm_flops;      /* 2*M*N*K summed over those launches */
+} lv_encoder_stats_t;
+
+typedef struct {
   int32_t arch;         /* 0 = BERT-style post-LN GELU, mean pool (C1-C3) */
   int32_t layers;
   int32_t hidden;
@@ -161,6 +174,14 @@ int lv_encoder_create(const lv_encoder_config *cfg, const float *const *weights,
 void lv_encoder_destroy(lv_encoder *enc);
 int lv_encode(lv_encoder *enc, const void *tokens, int32_t token_bytes, int64_t n_seqs,
               int32_t seq_len, float *out, int flags, void *stream);
+int lv_encoder_profile(lv_encoder *enc, int enable);
+int lv_encoder_stats(lv_encoder *enc, lv_encoder_stats_t *stats);
+int lv_encoder_reset_stats(lv_encoder *enc);
+
+/* out[M][N] = epi(A[M][K] . W[N][K]^T (+ bias) ...), bf16 device pointers, fp32 bias;
+ * epi: 0 bias, 1 bias + erf-GELU, 2 bias + residual. N % 128 == 0, K % 64 == 0. */
+int lv_gemm_bf16(const void *A, const void *W, const float *bias, const void *residual,
+                 void *out, int32_t M, int32_t N, int32_t K, int32_t epi, void *stream);
 
 #ifdef __cplusplus
 }

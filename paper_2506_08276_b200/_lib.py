@@ -64,6 +64,13 @@ class EncoderConfigC(C.Structure):
     ]
 
 
+class EncoderStats(C.Structure):
+    _fields_ = [
+        ("passages", C.c_int64), ("gemm_launches", C.c_int64),
+        ("gemm_ms", C.c_double), ("gemm_flops", C.c_double),
+    ]
+
+
 EXPORTS = {
     "lv_last_error": (C.c_char_p, []),
     "lv_version": (C.c_int, []),
@@ -86,6 +93,11 @@ EXPORTS = {
     "lv_encoder_create": (C.c_int, [C.POINTER(EncoderConfigC), C.POINTER(C.c_void_p), C.c_int32,
                                     C.c_int, C.POINTER(C.c_void_p)]),
     "lv_encoder_destroy": (None, [C.c_void_p]),
+    "lv_encoder_profile": (C.c_int, [C.c_void_p, C.c_int]),
+    "lv_encoder_stats": (C.c_int, [C.c_void_p, C.POINTER(EncoderStats)]),
+    "lv_encoder_reset_stats": (C.c_int, [C.c_void_p]),
+    "lv_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "lv_encode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_void_p,
                             C.c_int, C.c_void_p]),
 }

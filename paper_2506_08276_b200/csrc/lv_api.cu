@@ -120,17 +120,6 @@ struct lv_index {
 
 namespace {
 
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
 int upload(void *dst, const void *src, size_t bytes, bool src_on_device, cudaStream_t s) {
   if (bytes == 0) return LV_OK;
   LV_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes,

@@ -42,6 +42,18 @@ struct Status {
   } while (0)
 
 constexpr int kMaxLevels = 32;
+
+// Make `dev` current for the lifetime of the guard.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 constexpr int kCentroids = 256;  // pq.py:29 CENTROIDS_PER_SUBSPACE
 
 // ---------------------------------------------------------------------------

@@ -1,27 +1,578 @@
-// lv_encoder.cu — placeholder until the encoder lands.
+// lv_encoder.cu — the passage encoder behind the recompute source.
+//
+// The reference's provider boundary (provider.embed_batch, vectors.py:201-211,
+// called from ProviderSource.fetch, search.py:103-110) maps item payloads to
+// unit vectors. Here the payload of node v is its row of the token store
+// (items.dat with packed u16/u32 token ids) and the provider is
+// a random-init BERT-style encoder (post-LN, erf-GELU, mean-pool + L2 norm):
+//
+//   x = LN(tok[id] + pos[p])
+//   per layer: x = LN1(x + Wo.attn(Wqkv.x + b) + bo); x = LN2(x + W2.gelu(W1.x + b1) + b2)
+//   out = normalize(mean_p x)
+//
+// precision 1 (bf16): weights/activations bf16, fp32 accumulate/statistics;
+//   GEMMs on tcgen05 (lv_gemm_tc.cu), attention on tensor cores (lv_attn.cu).
+// precision 0 (fp32): SIMT fp32 GEMM and attention — the parity mode checked
+//   against the torch fp32 oracle (oracle/encoder_ref.py).
+// Both are batch-invariant: a passage's embedding never depends on the batch
+// it rides in (the test_vectors.py:145-152 contract).
+#include <cmath>
+#include <cstring>
+#include <vector>
+
 #include "lv_encoder.cuh"
+#include "lv_kernels.cuh"
+
+namespace lv {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr float kLnEps = 1e-12f;
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// One warp per token row: gather token + position embedding, LayerNorm.
+// Row r of sequence n reads token store row ids[n] (or n when ids is null).
+template <typename T>
+__global__ void embed_ln_kernel(const void *__restrict__ tokens, int token_bytes, int S,
+                                const int32_t *__restrict__ ids, int64_t seq0, int64_t n_seqs,
+                                const float *__restrict__ tok_emb, const float *__restrict__ pos_emb,
+                                int vocab, const float *__restrict__ g,
+                                const float *__restrict__ b, int d, T *__restrict__ out) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_seqs * S) return;
+  const int64_t n = seq0 + row / S;
+  const int p = (int)(row % S);
+  const int64_t src = ids ? (int64_t)__ldg(ids + n) : n;
+  uint32_t tok = token_bytes == 2
+                     ? (uint32_t)__ldg(reinterpret_cast<const uint16_t *>(tokens) + src * S + p)
+                     : __ldg(reinterpret_cast<const uint32_t *>(tokens) + src * S + p);
+  if (tok >= (uint32_t)vocab) tok = vocab - 1;  // ids are validated on the host path
+  const float *te = tok_emb + (size_t)tok * d;
+  const float *pe = pos_emb + (size_t)p * d;
+  float v[32];
+  const int per = d / 32;
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i < per) {
+      const int c = i * 32 + lane;
+      v[i] = __ldg(te + c) + __ldg(pe + c);
+      s += v[i];
+    }
+  }
+  const float mean = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < per) {
+      const float t = v[i] - mean;
+      q += t * t;
+    }
+  const float rstd = rsqrtf(warp_sum(q) / d + kLnEps);
+  T *o = out + row * d;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < per) {
+      const int c = i * 32 + lane;
+      o[c] = from_f<T>((v[i] - mean) * rstd * __ldg(g + c) + __ldg(b + c));
+    }
+}
+
+// out = LN(in), one warp per row.
+template <typename T>
+__global__ void ln_kernel(const T *__restrict__ in, T *__restrict__ out, const float *__restrict__ g,
+                          const float *__restrict__ b, int64_t rows, int d) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const T *x = in + row * d;
+  float v[32];
+  const int per = d / 32;
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < per) {
+      v[i] = to_f<T>(x[i * 32 + lane]);
+      s += v[i];
+    }
+  const float mean = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < per) {
+      const float t = v[i] - mean;
+      q += t * t;
+    }
+  const float rstd = rsqrtf(warp_sum(q) / d + kLnEps);
+  T *o = out + row * d;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < per) {
+      const int c = i * 32 + lane;
+      o[c] = from_f<T>((v[i] - mean) * rstd * __ldg(g + c) + __ldg(b + c));
+    }
+}
+
+// Mean over the S token rows of each sequence, then L2 normalisation
+// (x / max(||x||, 1e-12)). One block per sequence, fixed summation order.
+template <typename T>
+__global__ void pool_kernel(const T *__restrict__ x, float *__restrict__ out, int S, int d) {
+  __shared__ float red[32];
+  const int64_t seq = blockIdx.x;
+  const T *base = x + seq * S * d;
+  float local = 0.f;
+  float mv[4];
+  int nv = 0;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < S; ++p) s += to_f<T>(base[(size_t)p * d + c]);
+    s /= (float)S;
+    mv[nv++] = s;
+    local += s * s;
+  }
+  local = warp_sum(local);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = 1.0f / fmaxf(sqrtf(red[0]), 1e-12f);
+  nv = 0;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) out[seq * d + c] = mv[nv++] * inv;
+}
+
+// fp32 SIMT GEMM, 64x64 tile, 4x4 per thread; sequential fmaf over K.
+__global__ void __launch_bounds__(256)
+    f32_gemm_kernel(const float *__restrict__ A, const float *__restrict__ W,
+                    const float *__restrict__ bias, const float *__restrict__ res,
+                    float *__restrict__ out, int M, int N, int K, int epi) {
+  __shared__ float As[16][68], Ws[16][68];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 1024; i += 256) {
+      const int r = i >> 4, c = i & 15;
+      const int gm = m0 + r, gn = n0 + r, gk = k0 + c;
+      As[c][r] = (gm < M && gk < K) ? __ldg(A + (size_t)gm * K + gk) : 0.f;
+      Ws[c][r] = (gn < N && gk < K) ? __ldg(W + (size_t)gn * K + gk) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = As[kk][ty * 4 + i];
+        w[i] = Ws[kk][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx * 4 + j;
+      if (gn >= N) continue;
+      float v = acc[i][j] + bias[gn];
+      if (epi == EPI_BIAS_GELU) v = 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+      else if (epi == EPI_BIAS_RESIDUAL) v += res[(size_t)gm * N + gn];
+      out[(size_t)gm * N + gn] = v;
+    }
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float *__restrict__ in, __nv_bfloat16 *__restrict__ out,
+                                   int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __float2bfloat16_rn(in[i]);
+}
+
+}  // namespace
+
+cudaError_t f32_gemm(const float *A, const float *W, const float *bias, const float *residual,
+                     float *out, int M, int N, int K, int epi, cudaStream_t s) {
+  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  f32_gemm_kernel<<<grid, 256, 0, s>>>(A, W, bias, residual, out, M, N, K, epi);
+  return cudaGetLastError();
+}
+
+}  // namespace lv
+
+using namespace lv;
+
+struct EncLayer {
+  void *w_qkv = nullptr, *w_o = nullptr, *w_1 = nullptr, *w_2 = nullptr;
+  float *b_qkv = nullptr, *b_o = nullptr, *b_1 = nullptr, *b_2 = nullptr;
+  float *ln1_g = nullptr, *ln1_b = nullptr, *ln2_g = nullptr, *ln2_b = nullptr;
+};
 
 struct lv_encoder {
-  int hidden = 0;
+  lv_encoder_config cfg{};
+  int device = 0;
+  float *tok_emb = nullptr, *pos_emb = nullptr, *emb_g = nullptr, *emb_b = nullptr;
+  std::vector<EncLayer> layers;
+  std::vector<void *> allocs;
+  // activation workspace (element size 2 or 4), grown on demand
+  int64_t cap_tokens = 0;
+  void *x = nullptr, *qkv = nullptr, *ctx = nullptr, *y = nullptr, *h = nullptr;
+  // profiling of the dense GEMMs (lv_encoder_profile)
+  bool profile = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used;
+  std::vector<double> ev_flops;
+  double gemm_ms = 0.0, gemm_flops = 0.0;
+  int64_t gemm_launches = 0;
+  int64_t passages = 0;
+  ~lv_encoder() {
+    for (void *p : allocs) cudaFree(p);
+    cudaFree(x);
+    cudaFree(qkv);
+    cudaFree(ctx);
+    cudaFree(y);
+    cudaFree(h);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto &pr : ev_used) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  }
+  size_t esize() const { return cfg.precision == 1 ? 2 : 4; }
 };
 
 namespace lv {
-int encoder_hidden(const lv_encoder *enc) { return enc ? enc->hidden : 0; }
-int encode_node_rows(lv_encoder *, const void *, int, int, const int32_t *, int64_t, float *,
-                     cudaStream_t) {
-  set_error("encoder not available");
-  return LV_ERR_INTERNAL;
+namespace {
+
+int dev_alloc(lv_encoder *e, void **p, size_t bytes) {
+  LV_CHECK_CUDA(cudaMalloc(p, bytes));
+  e->allocs.push_back(*p);
+  return LV_OK;
 }
+
+int upload_f32(lv_encoder *e, float **dst, const float *src, size_t n) {
+  LV_TRY(dev_alloc(e, (void **)dst, n * 4));
+  LV_CHECK_CUDA(cudaMemcpy(*dst, src, n * 4, cudaMemcpyHostToDevice));
+  return LV_OK;
+}
+
+// matrices: bf16 copies for the tensor-core path, fp32 for parity mode
+int upload_mat(lv_encoder *e, void **dst, const float *src, size_t n) {
+  if (e->cfg.precision == 0) return upload_f32(e, (float **)dst, src, n);
+  float *tmp = nullptr;
+  LV_CHECK_CUDA(cudaMalloc(&tmp, n * 4));
+  LV_CHECK_CUDA(cudaMemcpy(tmp, src, n * 4, cudaMemcpyHostToDevice));
+  int rc = dev_alloc(e, dst, n * 2);
+  if (rc == LV_OK) {
+    f32_to_bf16_kernel<<<(unsigned)((n + 255) / 256), 256>>>(tmp, (__nv_bfloat16 *)*dst,
+                                                            (int64_t)n);
+    if (cudaDeviceSynchronize() != cudaSuccess) rc = LV_ERR_INTERNAL;
+  }
+  cudaFree(tmp);
+  return rc;
+}
+
+int ensure_ws(lv_encoder *e, int64_t tokens) {
+  if (tokens <= e->cap_tokens) return LV_OK;
+  cudaFree(e->x);
+  cudaFree(e->qkv);
+  cudaFree(e->ctx);
+  cudaFree(e->y);
+  cudaFree(e->h);
+  e->x = e->qkv = e->ctx = e->y = e->h = nullptr;
+  e->cap_tokens = 0;
+  const size_t es = e->esize();
+  const size_t d = e->cfg.hidden, ff = e->cfg.ffn;
+  LV_CHECK_CUDA(cudaMalloc(&e->x, tokens * d * es));
+  LV_CHECK_CUDA(cudaMalloc(&e->qkv, tokens * 3 * d * es));
+  LV_CHECK_CUDA(cudaMalloc(&e->ctx, tokens * d * es));
+  LV_CHECK_CUDA(cudaMalloc(&e->y, tokens * d * es));
+  LV_CHECK_CUDA(cudaMalloc(&e->h, tokens * ff * es));
+  e->cap_tokens = tokens;
+  return LV_OK;
+}
+
+cudaEvent_t take_event(lv_encoder *e) {
+  if (!e->ev_pool.empty()) {
+    cudaEvent_t ev = e->ev_pool.back();
+    e->ev_pool.pop_back();
+    return ev;
+  }
+  cudaEvent_t ev;
+  cudaEventCreate(&ev);
+  return ev;
+}
+
+template <typename T>
+int gemm(lv_encoder *e, const void *A, const void *W, const float *bias, const void *res, void *out,
+         int M, int N, int K, int epi, cudaStream_t s) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (e->profile) {
+    e0 = take_event(e);
+    e1 = take_event(e);
+    cudaEventRecord(e0, s);
+  }
+  if constexpr (sizeof(T) == 2) {
+    LV_TRY(tc_gemm((const __nv_bfloat16 *)A, (const __nv_bfloat16 *)W, bias,
+                   (const __nv_bfloat16 *)res, (__nv_bfloat16 *)out, M, N, K, epi, s));
+  } else {
+    LV_CHECK_CUDA(f32_gemm((const float *)A, (const float *)W, bias, (const float *)res,
+                           (float *)out, M, N, K, epi, s));
+  }
+  if (e->profile) {
+    cudaEventRecord(e1, s);
+    e->ev_used.emplace_back(e0, e1);
+    e->ev_flops.push_back(2.0 * M * (double)N * K);
+  }
+  return LV_OK;
+}
+
+template <typename T>
+int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int32_t *d_ids,
+            int64_t n_seqs, float *out, cudaStream_t s) {
+  const auto &c = e->cfg;
+  const int d = c.hidden, ff = c.ffn, H = c.heads, dh = c.hidden / c.heads;
+  const int64_t max_tokens = std::max<int64_t>(S, (int64_t)1 << 19);
+  const int64_t chunk = std::max<int64_t>(1, max_tokens / S);
+  LV_TRY(ensure_ws(e, std::min<int64_t>(n_seqs, chunk) * S));
+  T *x = (T *)e->x, *qkv = (T *)e->qkv, *ctx = (T *)e->ctx, *y = (T *)e->y, *h = (T *)e->h;
+  for (int64_t s0 = 0; s0 < n_seqs; s0 += chunk) {
+    const int64_t ns = std::min(chunk, n_seqs - s0);
+    const int M = (int)(ns * S);
+    embed_ln_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, s>>>(
+        tokens, token_bytes, S, d_ids, s0, ns, e->tok_emb, e->pos_emb, c.vocab, e->emb_g,
+        e->emb_b, d, x);
+    LV_CHECK_CUDA(cudaGetLastError());
+    for (const EncLayer &L : e->layers) {
+      LV_TRY(gemm<T>(e, x, L.w_qkv, L.b_qkv, nullptr, qkv, M, 3 * d, d, EPI_BIAS, s));
+      if constexpr (sizeof(T) == 2) {
+        LV_CHECK_CUDA(attention_bf16((const __nv_bfloat16 *)qkv, (__nv_bfloat16 *)ctx, (int)ns, S,
+                                     H, dh, s));
+      } else {
+        LV_CHECK_CUDA(attention_f32((const float *)qkv, (float *)ctx, (int)ns, S, H, dh, s));
+      }
+      LV_TRY(gemm<T>(e, ctx, L.w_o, L.b_o, x, y, M, d, d, EPI_BIAS_RESIDUAL, s));
+      ln_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, s>>>(y, x, L.ln1_g, L.ln1_b, M, d);
+      LV_TRY(gemm<T>(e, x, L.w_1, L.b_1, nullptr, h, M, ff, d, EPI_BIAS_GELU, s));
+      LV_TRY(gemm<T>(e, h, L.w_2, L.b_2, x, y, M, d, ff, EPI_BIAS_RESIDUAL, s));
+      ln_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, s>>>(y, x, L.ln2_g, L.ln2_b, M, d);
+    }
+    pool_kernel<T><<<(unsigned)ns, 256, 0, s>>>(x, out + s0 * d, S, d);
+    LV_CHECK_CUDA(cudaGetLastError());
+  }
+  e->passages += n_seqs;
+  return LV_OK;
+}
+
+}  // namespace
+
+int encoder_hidden(const lv_encoder *enc) { return enc ? enc->cfg.hidden : 0; }
+
+int encode_node_rows(lv_encoder *enc, const void *tokens, int token_bytes, int seq_len,
+                     const int32_t *d_ids, int64_t count, float *out, cudaStream_t s) {
+  LV_REQUIRE(enc, LV_ERR_USAGE, "null encoder");
+  LV_REQUIRE(seq_len <= enc->cfg.max_seq, LV_ERR_USAGE, "seq_len exceeds the encoder's max_seq");
+  if (count <= 0) return LV_OK;
+  if (enc->cfg.precision == 1)
+    return forward<__nv_bfloat16>(enc, tokens, token_bytes, seq_len, d_ids, count, out, s);
+  return forward<float>(enc, tokens, token_bytes, seq_len, d_ids, count, out, s);
+}
+
+// Resolve the recorded GEMM events (after the stream has been synchronised).
+void encoder_collect_profile(lv_encoder *enc) {
+  if (!enc) return;
+  for (size_t i = 0; i < enc->ev_used.size(); ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, enc->ev_used[i].first, enc->ev_used[i].second) == cudaSuccess) {
+      enc->gemm_ms += ms;
+      enc->gemm_flops += enc->ev_flops[i];
+      enc->gemm_launches += 1;
+    }
+    enc->ev_pool.push_back(enc->ev_used[i].first);
+    enc->ev_pool.push_back(enc->ev_used[i].second);
+  }
+  enc->ev_used.clear();
+  enc->ev_flops.clear();
+}
+
 }  // namespace lv
 
 extern "C" {
-int lv_encoder_create(const lv_encoder_config *, const float *const *, int32_t, int, lv_encoder **) {
-  lv::set_error("encoder not available");
-  return LV_ERR_INTERNAL;
+
+int lv_encoder_create(const lv_encoder_config *cfg, const float *const *weights, int32_t n_weights,
+                      int device, lv_encoder **out) {
+  LV_REQUIRE(cfg && weights && out, LV_ERR_USAGE, "lv_encoder_create: null argument");
+  *out = nullptr;
+  LV_REQUIRE(cfg->arch == 0, LV_ERR_USAGE, "only arch 0 (BERT-style) is supported");
+  LV_REQUIRE(cfg->precision == 0 || cfg->precision == 1, LV_ERR_USAGE, "precision must be 0 or 1");
+  LV_REQUIRE(cfg->layers >= 1 && cfg->heads >= 1 && cfg->hidden % cfg->heads == 0, LV_ERR_USAGE,
+             "bad encoder geometry");
+  LV_REQUIRE(cfg->hidden % 32 == 0 && cfg->hidden <= 1024, LV_ERR_USAGE,
+             "hidden must be a multiple of 32 and <= 1024");
+  LV_REQUIRE(cfg->vocab >= 1 && cfg->max_seq >= 1 && cfg->ffn >= 1, LV_ERR_USAGE,
+             "bad encoder geometry");
+  if (cfg->precision == 1) {
+    const int dh = cfg->hidden / cfg->heads;
+    LV_REQUIRE(cfg->hidden % 128 == 0 && cfg->ffn % 128 == 0 && (dh == 64 || dh == 128),
+               LV_ERR_USAGE, "bf16 encoder needs hidden, ffn % 128 == 0 and head dim 64/128");
+  }
+  LV_REQUIRE(n_weights == 4 + 12 * cfg->layers, LV_ERR_USAGE,
+             "weights: expected 4 + 12 * layers arrays");
+  DeviceGuard guard(device);
+  auto *e = new lv_encoder();
+  e->cfg = *cfg;
+  e->device = device;
+  const size_t d = cfg->hidden, ff = cfg->ffn;
+  int rc = LV_OK;
+  auto up = [&](float **dst, int idx, size_t n) {
+    if (rc == LV_OK) rc = upload_f32(e, dst, weights[idx], n);
+  };
+  auto upm = [&](void **dst, int idx, size_t n) {
+    if (rc == LV_OK) rc = upload_mat(e, dst, weights[idx], n);
+  };
+  up(&e->tok_emb, 0, (size_t)cfg->vocab * d);
+  up(&e->pos_emb, 1, (size_t)cfg->max_seq * d);
+  up(&e->emb_g, 2, d);
+  up(&e->emb_b, 3, d);
+  e->layers.resize(cfg->layers);
+  for (int l = 0; l < cfg->layers; ++l) {
+    EncLayer &L = e->layers[l];
+    const int b = 4 + 12 * l;
+    upm(&L.w_qkv, b + 0, 3 * d * d);
+    up(&L.b_qkv, b + 1, 3 * d);
+    upm(&L.w_o, b + 2, d * d);
+    up(&L.b_o, b + 3, d);
+    up(&L.ln1_g, b + 4, d);
+    up(&L.ln1_b, b + 5, d);
+    upm(&L.w_1, b + 6, ff * d);
+    up(&L.b_1, b + 7, ff);
+    upm(&L.w_2, b + 8, d * ff);
+    up(&L.b_2, b + 9, d);
+    up(&L.ln2_g, b + 10, d);
+    up(&L.ln2_b, b + 11, d);
+  }
+  if (rc != LV_OK) {
+    delete e;
+    return rc;
+  }
+  *out = e;
+  return LV_OK;
 }
-void lv_encoder_destroy(lv_encoder *enc) { delete enc; }
-int lv_encode(lv_encoder *, const void *, int32_t, int64_t, int32_t, float *, int, void *) {
-  lv::set_error("encoder not available");
-  return LV_ERR_INTERNAL;
+
+void lv_encoder_destroy(lv_encoder *enc) {
+  if (!enc) return;
+  DeviceGuard guard(enc->device);
+  delete enc;
 }
+
+int lv_encode(lv_encoder *enc, const void *tokens, int32_t token_bytes, int64_t n_seqs,
+              int32_t seq_len, float *out, int flags, void *stream) {
+  LV_REQUIRE(enc && tokens && out, LV_ERR_USAGE, "lv_encode: null argument");
+  LV_REQUIRE(token_bytes == 2 || token_bytes == 4, LV_ERR_USAGE, "token_bytes must be 2 or 4");
+  LV_REQUIRE(seq_len >= 1 && seq_len <= enc->cfg.max_seq, LV_ERR_USAGE,
+             "seq_len must be in [1, max_seq]");
+  if (enc->cfg.precision == 1)
+    LV_REQUIRE(seq_len % 64 == 0, LV_ERR_USAGE, "bf16 encoder needs seq_len % 64 == 0");
+  if (n_seqs <= 0) return LV_OK;
+  DeviceGuard guard(enc->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t tok_n = (size_t)n_seqs * seq_len;
+  if (flags & LV_IO_DEVICE)
+    return encode_node_rows(enc, tokens, token_bytes, seq_len, nullptr, n_seqs, out, s);
+  // host tokens: validate ids (the reference raises on bad payloads), stage, encode, copy back
+  for (size_t i = 0; i < tok_n; ++i) {
+    uint32_t t = token_bytes == 2 ? ((const uint16_t *)tokens)[i] : ((const uint32_t *)tokens)[i];
+    LV_REQUIRE(t < (uint32_t)enc->cfg.vocab, LV_ERR_DATA, "token id out of vocabulary");
+  }
+  void *dt = nullptr;
+  float *dout = nullptr;
+  LV_CHECK_CUDA(cudaMalloc(&dt, tok_n * token_bytes));
+  if (cudaMalloc(&dout, (size_t)n_seqs * enc->cfg.hidden * 4) != cudaSuccess) {
+    cudaFree(dt);
+    set_error("cudaMalloc failed");
+    return LV_ERR_INTERNAL;
+  }
+  int rc = LV_OK;
+  if (cudaMemcpyAsync(dt, tokens, tok_n * token_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    rc = LV_ERR_INTERNAL;
+  if (rc == LV_OK) rc = encode_node_rows(enc, dt, token_bytes, seq_len, nullptr, n_seqs, dout, s);
+  if (rc == LV_OK &&
+      cudaMemcpyAsync(out, dout, (size_t)n_seqs * enc->cfg.hidden * 4, cudaMemcpyDeviceToHost,
+                      s) != cudaSuccess)
+    rc = LV_ERR_INTERNAL;
+  if (cudaStreamSynchronize(s) != cudaSuccess && rc == LV_OK) {
+    set_error(std::string("encoder failed: ") + cudaGetErrorString(cudaGetLastError()));
+    rc = LV_ERR_INTERNAL;
+  }
+  cudaFree(dt);
+  cudaFree(dout);
+  return rc;
 }
+
+int lv_gemm_bf16(const void *A, const void *W, const float *bias, const void *residual, void *out,
+                 int32_t M, int32_t N, int32_t K, int32_t epi, void *stream) {
+  LV_REQUIRE(A && W && bias && out, LV_ERR_USAGE, "lv_gemm_bf16: null argument");
+  LV_REQUIRE(epi >= 0 && epi <= 2, LV_ERR_USAGE, "lv_gemm_bf16: unknown epilogue");
+  return tc_gemm((const __nv_bfloat16 *)A, (const __nv_bfloat16 *)W, bias,
+                 (const __nv_bfloat16 *)residual, (__nv_bfloat16 *)out, M, N, K, epi,
+                 (cudaStream_t)stream);
+}
+
+int lv_encoder_profile(lv_encoder *enc, int enable) {
+  LV_REQUIRE(enc, LV_ERR_USAGE, "null encoder");
+  enc->profile = enable != 0;
+  return LV_OK;
+}
+
+int lv_encoder_stats(lv_encoder *enc, lv_encoder_stats_t *st) {
+  LV_REQUIRE(enc && st, LV_ERR_USAGE, "null argument");
+  DeviceGuard guard(enc->device);
+  cudaDeviceSynchronize();
+  encoder_collect_profile(enc);
+  st->passages = enc->passages;
+  st->gemm_launches = enc->gemm_launches;
+  st->gemm_ms = enc->gemm_ms;
+  st->gemm_flops = enc->gemm_flops;
+  return LV_OK;
+}
+
+int lv_encoder_reset_stats(lv_encoder *enc) {
+  LV_REQUIRE(enc, LV_ERR_USAGE, "null encoder");
+  DeviceGuard guard(enc->device);
+  cudaDeviceSynchronize();
+  encoder_collect_profile(enc);
+  enc->passages = 0;
+  enc->gemm_launches = 0;
+  enc->gemm_ms = 0.0;
+  enc->gemm_flops = 0.0;
+  return LV_OK;
+}
+
+}  // extern "C"

@@ -11,4 +11,8 @@ int encoder_hidden(const lv_encoder *enc);
 int encode_node_rows(lv_encoder *enc, const void *tokens, int token_bytes, int seq_len,
                      const int32_t *d_ids, int64_t count, float *out, cudaStream_t s);
 
+// Fold the GEMM events recorded in profile mode into the encoder's counters
+// (call after the launching stream has been synchronised).
+void encoder_collect_profile(lv_encoder *enc);
+
 }  // namespace lv

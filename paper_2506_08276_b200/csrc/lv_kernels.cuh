@@ -1,0 +1,39 @@
+// lv_kernels.cuh — launchers of the passage-encoder kernels (lv_encoder.cu,
+// lv_gemm_tc.cu, lv_attn.cu). Activations are token-major [T][width] with
+// T = n_seqs * seq_len; every kernel is batch-invariant (a row's result never
+// depends on which other rows share the launch): fixed K order, no split-K.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "lv_common.cuh"
+
+namespace lv {
+
+enum Epi : int {
+  EPI_BIAS = 0,           // out = acc + bias
+  EPI_BIAS_GELU = 1,      // out = gelu_erf(acc + bias)
+  EPI_BIAS_RESIDUAL = 2,  // out = acc + bias + residual
+};
+
+// ---- bf16 tcgen05 GEMM (lv_gemm_tc.cu): out[M][N] = epi(A[M][K] . W[N][K]^T)
+// A, W, residual, out bf16 row-major; bias fp32. Requires N % 128 == 0,
+// K % 64 == 0, 16-byte aligned rows. Persistent, warp-specialised:
+// TMA producer / single-thread tcgen05.mma issuer / 4 epilogue warps.
+struct TcGemmPlan;  // cached tensor maps for one (A, W, M, N, K)
+int tc_gemm(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
+            const __nv_bfloat16 *residual, __nv_bfloat16 *out, int M, int N, int K, int epi,
+            cudaStream_t s);
+int tc_gemm_num_sms();
+
+// ---- fp32 SIMT GEMM (parity mode, lv_encoder.cu): same contract in fp32.
+cudaError_t f32_gemm(const float *A, const float *W, const float *bias, const float *residual,
+                     float *out, int M, int N, int K, int epi, cudaStream_t s);
+
+// ---- attention (lv_attn.cu). qkv [T][3*H*dh] (q | k | v, head-major inside
+// each), out [T][H*dh]; bidirectional softmax(q k^T / sqrt(dh)) v per sequence.
+cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S,
+                           int H, int dh, cudaStream_t s);
+cudaError_t attention_f32(const float *qkv, float *out, int n_seqs, int S, int H, int dh,
+                          cudaStream_t s);
+
+}  // namespace lv

@@ -1,0 +1,119 @@
+"""GPU numerics of the passage encoder and its tcgen05 GEMM against plain
+PyTorch fp32 references (oracle/encoder_ref.py), plus batch invariance."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lv():
+    import __graft_entry__ as ge
+    ge.build()
+    import paper_2506_08276_b200 as mod
+    return mod
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@pytest.mark.parametrize("M,N,K,epi", [
+    (128, 256, 64, 0), (1000, 768, 768, 0), (777, 2304, 768, 0), (640, 3072, 768, 1),
+    (513, 768, 3072, 2), (300, 128, 256, 2), (4096, 1024, 256, 1), (129, 384, 512, 0),
+])
+def test_tc_gemm_matches_torch(lv, M, N, K, epi):
+    torch = _torch()
+    from paper_2506_08276_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g) * 0.1
+    res = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().lv_gemm_bf16(A.data_ptr(), W.data_ptr(), bias.data_ptr(),
+                                       res.data_ptr(), out.data_ptr(), M, N, K, epi,
+                                       torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    ref = A.float() @ W.float().T + bias
+    if epi == 1:
+        ref = torch.nn.functional.gelu(ref)
+    elif epi == 2:
+        ref = ref + res.float()
+    err = (out.float() - ref).abs()
+    tol = 2e-2 * ref.abs() + 2e-2  # bf16 output rounding (2^-8 relative) + fp32 order
+    assert bool((err <= tol).all()), float(err.max())
+
+
+def _small_cfg(lv, layers=2):
+    from paper_2506_08276_b200.encoder import EncoderConfig
+    return EncoderConfig("test-2l-d256", layers, 256, 4, 1024, 30522, 256)
+
+
+def test_encoder_fp32_matches_torch(lv):
+    from oracle.encoder_ref import RefEncoder
+    from paper_2506_08276_b200.encoder import GpuEncoder, init_weights, synthetic_tokens
+    cfg = _small_cfg(lv)
+    w = init_weights(cfg, seed=3)
+    tok = synthetic_tokens(24, 128, cfg.vocab, seed=5)
+    got = GpuEncoder(cfg, w, precision="fp32").encode(tok)
+    ref = RefEncoder(cfg, w).encode(tok)
+    np.testing.assert_allclose(got, ref, rtol=0, atol=2e-5)
+
+
+def test_encoder_bf16_close_to_torch(lv):
+    from oracle.encoder_ref import RefEncoder
+    from paper_2506_08276_b200.encoder import GpuEncoder, init_weights, synthetic_tokens
+    cfg = _small_cfg(lv)
+    w = init_weights(cfg, seed=3)
+    tok = synthetic_tokens(40, 128, cfg.vocab, seed=6)
+    got = GpuEncoder(cfg, w, precision="bf16").encode(tok)
+    ref = RefEncoder(cfg, w).encode(tok)
+    cos = (got * ref).sum(1) / np.linalg.norm(got, axis=1) / np.linalg.norm(ref, axis=1)
+    assert cos.min() > 0.995, cos.min()
+
+
+def test_encoder_bert_base_bf16_close_to_torch(lv):
+    from oracle.encoder_ref import RefEncoder
+    from paper_2506_08276_b200.encoder import ENCODERS, GpuEncoder, init_weights, synthetic_tokens
+    cfg = ENCODERS["bert-base"]
+    w = init_weights(cfg, seed=11)
+    tok = synthetic_tokens(6, 256, cfg.vocab, seed=12)
+    got = GpuEncoder(cfg, w, precision="bf16").encode(tok)
+    ref = RefEncoder(cfg, w).encode(tok)
+    cos = (got * ref).sum(1)
+    assert cos.min() > 0.99, cos.min()
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_encoder_batch_invariant(lv, precision):
+    """embed_all split is value-neutral (test_vectors.py:145-152): bitwise."""
+    from paper_2506_08276_b200.encoder import GpuEncoder, init_weights, synthetic_tokens
+    cfg = _small_cfg(lv)
+    enc = GpuEncoder(cfg, init_weights(cfg, seed=1), precision=precision)
+    tok = synthetic_tokens(37, 128, cfg.vocab, seed=2)
+    whole = enc.encode(tok)
+    parts = np.concatenate([enc.encode(tok[:1]), enc.encode(tok[1:20]), enc.encode(tok[20:])])
+    assert np.array_equal(whole, parts)
+    assert np.array_equal(enc.encode(tok[5:6])[0], whole[5])
+
+
+def test_encoder_device_tokens_and_provider(lv):
+    torch = _torch()
+    from paper_2506_08276_b200.encoder import (EncoderProvider, GpuEncoder, TokenStore,
+                                               init_weights, synthetic_tokens)
+    from collections import namedtuple
+    EmbeddingRequest = namedtuple("EmbeddingRequest", "item_id content")  # vectors.py:33-38
+    cfg = _small_cfg(lv)
+    enc = GpuEncoder(cfg, init_weights(cfg, seed=1), precision="bf16")
+    tok = synthetic_tokens(10, 128, cfg.vocab, seed=9)
+    host = enc.encode(tok)
+    dev = enc.encode(torch.from_numpy(tok.astype(np.int16)).cuda()).cpu().numpy()
+    assert np.array_equal(host, dev)
+    prov = EncoderProvider(enc, TokenStore(tok))
+    store = TokenStore(tok)
+    reqs = [EmbeddingRequest(i, store.get(i)) for i in (3, 7)]
+    assert np.array_equal(prov.embed_batch(reqs), host[[3, 7]])
