@@ -157,6 +157,8 @@ int lv_index_set_cache(lv_index *index, const int64_t *ids, int64_t count, int f
 int lv_index_attach_encoder(lv_index *index, lv_encoder *enc, const void *tokens,
                             int32_t token_bytes, int32_t seq_len, int flags);
 
+/* qnorm may be NULL: norms are then computed on the device (not bit-identical to
+ * the reference's host np.dot, vectors.py:138 — parity callers pass qnorm). */
 int lv_search_batch(lv_index *index, const float *q, const float *qnorm, int32_t B,
                     const lv_search_params *params, const lv_search_outputs *out,
                     void *stream);

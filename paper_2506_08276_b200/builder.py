@@ -1,0 +1,342 @@
+"""GPU index construction: LGR1 pruned graph + LPQ1 PQ artefacts from an embedding matrix.
+
+Measurement infrastructure for the search hot path: the
+reference builder (builder.py:499-548) inserts nodes one at a time in Python
+and needs ~3.8 h at 1M nodes, so configs 2-5 cannot use it. This builder keeps
+its structure and rules, batched on the GPU with PyTorch:
+
+* levels: the reference's keyed geometric draw ``assign_level`` (builder.py:83-96);
+  entry point = lowest id at the top level (the first such node the
+  reference inserts);
+* per level: exact k-NN candidates among that level's nodes (bf16 GEMM tiles,
+  exact fp32 re-rank) in place of the HNSW ``_search_layer`` candidate pool;
+* relative-neighbourhood selection (``rng_shrink``, builder.py:99-118) of the
+  candidates, then backlinks with shrink-to-M (``_Inserter.insert``,
+  builder.py:367-402);
+* two passes with hub preservation: pass 1 at the uniform cap M gives the
+  degrees, ``select_hubs`` (builder.py:121-127) picks the top beta%, pass 2
+  inserts hubs at cap M and everyone else at m = M // 5 (builder.py:499-548);
+* PQ: per-subspace k-means++ (PCG64 seed + s) and fixed iterations on the
+  first-100k sample, nearest-centroid codes (pq.py:79-136, cluster.py:15-64).
+
+Search parity does not depend on this builder: both the reference search and
+the device search read the same files it writes.
+"""
+from __future__ import annotations
+
+import hashlib
+import math
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from .graph import PrunedGraph
+from .pq import PQCodes, PQModel, default_m_pq
+
+_MAX_LEVEL = 24           # builder.py:36
+_PQ_SAMPLE_CAP = 100_000  # builder.py:38
+
+
+@dataclass
+class GpuBuildParams:
+    """builder.py:42-69 knobs used by the batched builder."""
+
+    max_degree: int = 32
+    low_degree: int | None = None
+    hub_percent: float = 2.0
+    metric: str = "cosine"
+    seed: int = 0
+    pq_subspaces: int | None = None
+    pq_iters: int = 10
+    candidates: int = 64      # k-NN pool per node (plays ef_construction's role)
+
+    def __post_init__(self) -> None:
+        if self.low_degree is None:
+            self.low_degree = max(1, self.max_degree // 5)
+
+
+def assign_level(node_id: int, seed: int, max_degree: int) -> int:
+    """Keyed geometric level draw, ratio 1/ln(M) (builder.py:83-96)."""
+    key = struct.pack("<Q", seed & 0xFFFFFFFFFFFFFFFF)
+    digest = hashlib.blake2b(b"level:%d" % node_id, digest_size=8, key=key).digest()
+    (word,) = struct.unpack("<Q", digest)
+    u = ((word >> 11) + 1) / float(2 ** 53)
+    return min(int(-math.log(u) / math.log(max_degree)), _MAX_LEVEL)
+
+
+def select_hubs(degrees: np.ndarray, hub_percent: float, n: int) -> np.ndarray:
+    """Top ceil(beta*n/100) ids by (degree desc, id asc) (builder.py:121-127)."""
+    count = min(n, math.ceil(hub_percent / 100.0 * n))
+    order = np.lexsort((np.arange(n), -np.asarray(degrees, dtype=np.int64)))
+    return np.sort(order[:count])
+
+
+def _prep(x, metric):
+    import torch
+    x = x.float()
+    if metric == "cosine":
+        x = x / x.norm(dim=1, keepdim=True).clamp_min(1e-30)
+    return x
+
+
+def _pair_dist(a, b, metric):
+    """Distances between matching rows (a, b: [..., d])."""
+    if metric == "l2":
+        d = a - b
+        return (d * d).sum(-1)
+    return -(a * b).sum(-1)
+
+
+def _knn(x, k: int, metric: str, chunk: int = 4096):
+    """Exact k nearest (excluding self) of every row of x among x: bf16 GEMM
+    candidates (k + 8 of them), re-ranked with fp32 distances."""
+    import torch
+    n = x.shape[0]
+    kk = min(n - 1, k)
+    extra = min(n - 1, kk + 8)
+    xb = x.to(torch.bfloat16)
+    sq = (x * x).sum(1) if metric == "l2" else None
+    ids = torch.empty((n, kk), dtype=torch.int64, device=x.device)
+    dist = torch.empty((n, kk), dtype=torch.float32, device=x.device)
+    ar = torch.arange(n, device=x.device)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        sc = (xb[s:e] @ xb.T).float()
+        if metric == "l2":
+            sc = 2 * sc - sq[None, :]
+        sc[torch.arange(e - s, device=x.device), ar[s:e]] = -float("inf")
+        cand = sc.topk(extra, dim=1).indices
+        dd = _pair_dist(x[s:e, None, :], x[cand], metric)
+        dd = torch.where(cand == ar[s:e, None], torch.full_like(dd, float("inf")), dd)
+        # (distance, id) ascending
+        order = torch.argsort(cand, dim=1)
+        cand = cand.gather(1, order)
+        dd = dd.gather(1, order)
+        order = torch.argsort(dd, dim=1, stable=True)
+        ids[s:e] = cand.gather(1, order)[:, :kk]
+        dist[s:e] = dd.gather(1, order)[:, :kk]
+    return ids, dist
+
+
+def _rng_select(x, cand, cdist, caps, metric, chunk: int = 8192):
+    """Relative-neighbourhood selection (rng_shrink, builder.py:99-118), batched:
+    candidates per owner sorted ascending by (distance, id), -1 padded; keep c
+    iff no kept k has dist(c, k) < dist(c, owner); stop at the owner's cap."""
+    import torch
+    B, R = cand.shape
+    keep = torch.zeros((B, R), dtype=torch.bool, device=x.device)
+    for s in range(0, B, chunk):
+        e = min(B, s + chunk)
+        c = cand[s:e]
+        valid = c >= 0
+        v = x[c.clamp_min(0)]                                  # [b, R, d]
+        if metric == "l2":
+            sq = (v * v).sum(-1)
+            pair = sq[:, :, None] + sq[:, None, :] - 2 * torch.bmm(v, v.transpose(1, 2))
+        else:
+            pair = -torch.bmm(v, v.transpose(1, 2))
+        d = cdist[s:e]
+        cap = caps[s:e]
+        kept = torch.zeros_like(valid)
+        cnt = torch.zeros(e - s, dtype=torch.int32, device=x.device)
+        for j in range(R):
+            blocked = (kept & (pair[:, j, :] < d[:, j:j + 1])).any(1)
+            take = valid[:, j] & ~blocked & (cnt < cap)
+            kept[:, j] = take
+            cnt += take.int()
+        keep[s:e] = kept
+    return keep
+
+
+def _level_graph(x_all, members, caps_all, M, metric, k, knn=None):
+    """One level: candidates -> RNG forward selection -> backlinks + shrink to M.
+    Returns (offsets u64[n+1], neighbours u32[nnz]) over all n nodes."""
+    import torch
+    n = x_all.shape[0]
+    dev = x_all.device
+    nm = members.shape[0]
+    if nm <= 1:
+        return np.zeros(n + 1, dtype=np.uint64), np.zeros(0, dtype=np.uint32)
+    x = x_all[members]
+    lid, ldist = knn if knn is not None else _knn(x, k, metric)
+    caps = caps_all[members]
+    keep = _rng_select(x, lid, ldist, caps, metric)
+    # forward edges (local ids) + backlinks
+    own = torch.arange(nm, device=dev)[:, None].expand_as(lid)
+    src = own[keep]
+    dst = lid[keep]
+    d = ldist[keep]
+    osrc = torch.cat([src, dst])
+    odst = torch.cat([dst, src])
+    od = torch.cat([d, d])
+    key = osrc * nm + odst
+    key, inv = torch.unique(key, return_inverse=True)
+    first = torch.full((key.shape[0],), -1, dtype=torch.int64, device=dev)
+    first.scatter_reduce_(0, inv, torch.arange(inv.shape[0], device=dev), reduce="amin",
+                          include_self=False)
+    osrc, odst, od = osrc[first], odst[first], od[first]
+    # sort by (owner, distance, id)
+    order = torch.argsort(odst, stable=True)
+    osrc, odst, od = osrc[order], odst[order], od[order]
+    order = torch.argsort(od, stable=True)
+    osrc, odst, od = osrc[order], odst[order], od[order]
+    order = torch.argsort(osrc, stable=True)
+    osrc, odst, od = osrc[order], odst[order], od[order]
+    counts = torch.bincount(osrc, minlength=nm)
+    starts = torch.cumsum(counts, 0) - counts
+    rank = torch.arange(osrc.shape[0], device=dev) - starts[osrc]
+    Rmax = 3 * M
+    sel = rank < Rmax
+    mat = torch.full((nm, Rmax), -1, dtype=torch.int64, device=dev)
+    mdist = torch.full((nm, Rmax), float("inf"), device=dev)
+    mat[osrc[sel], rank[sel]] = odst[sel]
+    mdist[osrc[sel], rank[sel]] = od[sel]
+    over = counts > M
+    final = mat >= 0
+    if bool(over.any()):
+        rows = torch.nonzero(over).squeeze(1)
+        kk = _rng_select(x, mat[rows], mdist[rows],
+                         torch.full((rows.shape[0],), M, dtype=torch.int32, device=dev), metric)
+        final[rows] = kk
+    deg = final.sum(1)
+    nb_local = mat[final]                      # row-major: grouped by owner, ascending distance
+    nb = members[nb_local]
+    deg_all = torch.zeros(n, dtype=torch.int64, device=dev)
+    deg_all[members] = deg
+    offs = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    offs[1:] = torch.cumsum(deg_all, 0)
+    # owners in member order == ascending global id (members is sorted)
+    return offs.cpu().numpy().astype(np.uint64), nb.cpu().numpy().astype(np.uint32)
+
+
+def build_graph_gpu(matrix, params: GpuBuildParams) -> PrunedGraph:
+    """Two-pass hub-preserving pruned graph over ``matrix`` (CUDA tensor [n, d])."""
+    import torch
+    n = matrix.shape[0]
+    dev = matrix.device
+    x = _prep(matrix, params.metric)
+    M, m = params.max_degree, params.low_degree
+    levels = np.array([assign_level(v, params.seed, M) for v in range(n)], dtype=np.uint16)
+    top = int(levels.max())
+    entry = int(np.flatnonzero(levels == top)[0])
+    base = torch.arange(n, device=dev)
+    full_caps = torch.full((n,), M, dtype=torch.int32, device=dev)
+    # pass 1 (uniform cap) -> degrees -> hubs
+    knn0 = _knn(x, params.candidates, params.metric)
+    offs1, _ = _level_graph(x, base, full_caps, M, params.metric, params.candidates, knn0)
+    degrees = np.diff(offs1.astype(np.int64))
+    hubs = select_hubs(degrees, params.hub_percent, n)
+    caps = torch.full((n,), m, dtype=torch.int32, device=dev)
+    caps[torch.from_numpy(hubs).to(dev)] = M
+    offsets, neighbors = [], []
+    for lvl in range(top + 1):
+        if lvl == 0:
+            o, nb = _level_graph(x, base, caps, M, params.metric, params.candidates, knn0)
+        else:
+            mem = torch.from_numpy(np.flatnonzero(levels >= lvl)).to(dev)
+            o, nb = _level_graph(x, mem, full_caps, M, params.metric, params.candidates)
+        offsets.append(o)
+        neighbors.append(nb)
+    return PrunedGraph(n=n, max_degree=M, entry_point=entry, levels=levels,
+                       level_offsets=offsets, level_neighbors=neighbors)
+
+
+def _kmeanspp_init(x, k: int, seed: int):
+    """cluster.py:48-64 on the GPU (one subspace)."""
+    import torch
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n = x.shape[0]
+    cent = torch.empty((k, x.shape[1]), dtype=torch.float32, device=x.device)
+    first = int(rng.integers(0, n))
+    cent[0] = x[first]
+    min_sq = ((x - cent[0]) ** 2).sum(1).double()
+    for c in range(1, k):
+        total = float(min_sq.sum())
+        if total <= 0.0:
+            cent[c:] = cent[c - 1]
+            break
+        target = rng.random() * total
+        idx = int(torch.searchsorted(torch.cumsum(min_sq, 0), torch.tensor(
+            [target], dtype=torch.float64, device=x.device)).item())
+        idx = min(idx, n - 1)
+        cent[c] = x[idx]
+        torch.minimum(min_sq, ((x - cent[c]) ** 2).sum(1).double(), out=min_sq)
+    return cent
+
+
+def train_pq_gpu(matrix, m_pq: int | None, metric: str, iters: int = 10, seed: int = 0,
+                 sample_cap: int = _PQ_SAMPLE_CAP):
+    """pq_train + pq_encode (pq.py:79-136) batched over subspaces on the GPU."""
+    import torch
+    n, dim = matrix.shape
+    m_pq = m_pq or default_m_pq(dim)
+    padded = dim if dim % m_pq == 0 else dim + (m_pq - dim % m_pq)
+    sub = padded // m_pq
+    x = torch.zeros((n, padded), dtype=torch.float32, device=matrix.device)
+    x[:, :dim] = matrix.float()
+    sample = x[:min(n, sample_cap)]
+    if sample.shape[0] < 256:
+        reps = -(-256 // sample.shape[0])
+        sample = sample.repeat(reps, 1)[:256]
+    xs = sample.view(sample.shape[0], m_pq, sub).transpose(0, 1).contiguous()  # [m, Ns, sub]
+    cbs = torch.stack([_kmeanspp_init(xs[s], 256, seed + s) for s in range(m_pq)])
+    for _ in range(iters):
+        cn = (cbs * cbs).sum(-1)                                   # [m, 256]
+        assign = torch.argmin(cn[:, None, :] - 2.0 * torch.bmm(xs, cbs.transpose(1, 2)), dim=2)
+        sums = torch.zeros_like(cbs, dtype=torch.float64)
+        cnt = torch.zeros(cbs.shape[:2], dtype=torch.float64, device=x.device)
+        sums.scatter_add_(1, assign[:, :, None].expand(-1, -1, sub), xs.double())
+        cnt.scatter_add_(1, assign, torch.ones_like(assign, dtype=torch.float64))
+        upd = (sums / cnt.clamp_min(1)[:, :, None]).float()
+        cbs = torch.where(cnt[:, :, None] > 0, upd, cbs)
+    codes = torch.empty((n, m_pq), dtype=torch.uint8, device=x.device)
+    cn = (cbs * cbs).sum(-1)
+    for s0 in range(0, n, 65536):
+        blk = x[s0:s0 + 65536].view(-1, m_pq, sub).transpose(0, 1)
+        d = cn[:, None, :] - 2.0 * torch.bmm(blk, cbs.transpose(1, 2))
+        codes[s0:s0 + 65536] = torch.argmin(d, dim=2).transpose(0, 1).to(torch.uint8)
+    model = PQModel(dim=dim, padded_dim=padded, m_pq=m_pq, metric=metric,
+                    codebooks=cbs.cpu().numpy().astype(np.float32))
+    return model, PQCodes(codes=codes.cpu().numpy())
+
+
+def brute_force_topk(matrix, queries, k: int, metric: str, deleted=None, chunk: int = 1024):
+    """evaluation.py:82-95 on the GPU in fp32: k smallest (distance, id) over active rows."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        E = matrix.float()
+        Q = torch.as_tensor(queries, dtype=torch.float32, device=E.device)
+        if metric == "cosine":
+            rn = E.norm(dim=1)
+        out = np.empty((Q.shape[0], k), dtype=np.int64)
+        for s in range(0, Q.shape[0], chunk):
+            q = Q[s:s + chunk]
+            dots = q @ E.T
+            if metric == "cosine":
+                d = -(dots / (rn[None, :] * q.norm(dim=1, keepdim=True)))
+            elif metric == "ip":
+                d = -dots
+            else:
+                d = (q * q).sum(1, keepdim=True) + (E * E).sum(1)[None, :] - 2 * dots
+            if deleted is not None:
+                d[:, torch.as_tensor(deleted, device=E.device)] = float("inf")
+            cand = d.topk(k + 8, dim=1, largest=False)
+            ci, cd = cand.indices, cand.values
+            order = torch.argsort(ci, dim=1)
+            ci, cd = ci.gather(1, order), cd.gather(1, order)
+            order = torch.argsort(cd, dim=1, stable=True)
+            out[s:s + chunk] = ci.gather(1, order)[:, :k].cpu().numpy()
+        return out
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def mean_recall(results, truth) -> float:
+    """evaluation.py:108-118: |found ∩ truth| / k averaged over queries."""
+    tot = 0.0
+    for got, gt in zip(results, truth):
+        tot += len(set(int(i) for i in got) & set(int(i) for i in gt)) / len(gt)
+    return tot / len(truth)

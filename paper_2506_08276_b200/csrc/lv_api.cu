@@ -543,9 +543,14 @@ extern "C" int lv_search_batch(lv_index *ix, const float *q, const float *qnorm,
     LV_TRY(upload(ws.q.ptr, q, (size_t)B * ix->dim * 4, false, s));
     d_q = ws.q.ptr;
   }
-  LV_REQUIRE(qnorm, LV_ERR_USAGE,
-             "qnorm is required: np.float32(np.sqrt(np.dot(q, q))) per query (vectors.py:138)");
-  if (!dev_io) {
+  if (!qnorm) {
+    // qn on the device (sequential fp32 sum of squares). Bit parity with the
+    // reference needs the host value np.float32(np.sqrt(np.dot(q, q)))
+    // (vectors.py:138, BLAS sdot order), so parity callers pass qnorm.
+    LV_TRY(ws.qn.ensure(B));
+    LV_CHECK_CUDA(launch_qnorm(d_q, B, ix->dim, ws.qn.ptr, s));
+    d_qn = ws.qn.ptr;
+  } else if (!dev_io) {
     LV_TRY(ws.qn.ensure(B));
     LV_TRY(upload(ws.qn.ptr, qnorm, (size_t)B * 4, false, s));
     d_qn = ws.qn.ptr;

@@ -636,6 +636,14 @@ __global__ void dist_kernel(int metric, const float *__restrict__ rows, int64_t 
     out[r] = finish_distance(metric, einsum_combine(a0, a1, a2, a3), einsum_combine(b0, b1, b2, b3), qn);
 }
 
+__global__ void qnorm_kernel(const float *__restrict__ q, int B, int dim, float *__restrict__ qn) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  float acc = 0.f;
+  for (int j = 0; j < dim; ++j) acc = __fadd_rn(acc, __fmul_rn(q[(int64_t)i * dim + j], q[(int64_t)i * dim + j]));
+  qn[i] = __fsqrt_rn(acc);
+}
+
 __global__ void slot_reset_kernel(SlotState *st, int slots) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= slots) return;
@@ -660,6 +668,12 @@ cudaError_t launch_frontier(const SearchCtx &ctx, cudaStream_t s) {
   }
   int blocks = (ctx.slots + kWarpsPerBlock - 1) / kWarpsPerBlock;
   frontier_kernel<<<blocks, kWarpsPerBlock * 32, smem, s>>>(ctx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_qnorm(const float *q, int B, int dim, float *qn, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  qnorm_kernel<<<(B + 127) / 128, 128, 0, s>>>(q, B, dim, qn);
   return cudaGetLastError();
 }
 

@@ -99,6 +99,7 @@ cudaError_t launch_adc_score(const float *lut, int m, const uint8_t *codes, cons
                              int64_t count, float *out, cudaStream_t s);
 cudaError_t launch_distance_many(int metric, const float *rows, int64_t nrows, int dim,
                                  const float *q, float qn, float *out, cudaStream_t s);
+cudaError_t launch_qnorm(const float *q, int B, int dim, float *qn, cudaStream_t s);
 cudaError_t launch_slot_reset(SlotState *st, int slots, cudaStream_t s);
 cudaError_t launch_frontier(const SearchCtx &ctx, cudaStream_t s);
 size_t frontier_smem_bytes(const SearchCtx &ctx);

@@ -349,6 +349,54 @@ class DeviceIndex:
             reports.append(rep)
         return reports
 
+    def search_device(self, Q, params: SearchParams, source, qn=None,
+                      cache: EmbeddingCache | None = None, max_inflight: int = 0,
+                      out: dict | None = None):
+        """Device-resident batch search: ``Q`` is a CUDA float32 tensor [B, dim],
+        ``qn`` a CUDA tensor [B] or None (norms then computed on the device).
+        Returns CUDA tensors ids [B, k] (int64, -1 padded), dist [B, k],
+        count [B], counters [B, 4] (recomputations, approx_lookups, cache_hits,
+        expansions). Stream-ordered on the current torch stream."""
+        import torch
+        if not (Q.is_cuda and Q.dtype == torch.float32 and Q.is_contiguous() and Q.dim() == 2):
+            raise InvalidArgumentError("Q must be a contiguous CUDA float32 [B, dim] tensor")
+        if Q.shape[1] != self.dim:
+            raise InvalidArgumentError(f"dimension mismatch: {Q.shape[1]} vs {self.dim}")
+        B, k = Q.shape[0], params.k
+        p = _lib.SearchParamsC()
+        p.k, p.ef = k, params.ef
+        p.rerank_percent = float(params.rerank_percent)
+        p.batch_size = params.batch_size
+        p.mode = _lib.LV_MODE[params.mode]
+        p.max_inflight = max_inflight
+        p.flags = _lib.LV_IO_DEVICE
+        if isinstance(source, MatrixSource):
+            p.source = _lib.LV_SOURCE_MATRIX
+            self.set_matrix(source.matrix)
+        elif isinstance(source, ProviderSource):
+            p.source = _lib.LV_SOURCE_ENCODER
+            self.attach_encoder(source.provider)
+        else:
+            raise InvalidArgumentError("source must be MatrixSource or ProviderSource")
+        self.set_cache(cache)
+        p.use_cache = 1 if cache is not None else 0
+        dev = Q.device
+        if out is None or out["ids"].shape[0] < B or out["ids"].shape[1] != k:
+            out = dict(ids=torch.empty((B, k), dtype=torch.int64, device=dev),
+                       dist=torch.empty((B, k), dtype=torch.float32, device=dev),
+                       count=torch.empty(B, dtype=torch.int32, device=dev),
+                       counters=torch.empty((B, 4), dtype=torch.int64, device=dev),
+                       status=torch.empty(B, dtype=torch.int32, device=dev))
+        o = _lib.SearchOutputs()
+        o.ids, o.dist = out["ids"].data_ptr(), out["dist"].data_ptr()
+        o.count, o.counters = out["count"].data_ptr(), out["counters"].data_ptr()
+        o.status = out["status"].data_ptr()
+        st = torch.cuda.current_stream(dev).cuda_stream
+        qp = None if qn is None else qn.data_ptr()
+        _lib.check(_lib.lib().lv_search_batch(self.handle, Q.data_ptr(), qp, B, C.byref(p),
+                                              C.byref(o), st))
+        return out
+
     def last_stats(self) -> dict:
         st = _lib.SearchStats()
         _lib.check(_lib.lib().lv_last_search_stats(self.handle, C.byref(st)))
