@@ -125,7 +125,7 @@ typedef struct {
   double frontier_ms;        /* device time in frontier kernels */
   double encoder_ms;         /* device time in the encoder */
   double total_ms;
-  int64_t adc_bytes;         /* algorithmic bytes of ADC+gather */
+  int64_t adc_bytes;         /* algorithmic bytes of the frontier kernels */
 } lv_search_stats;
 
 typedef struct {
@@ -148,6 +148,8 @@ typedef struct {
 
 const char *lv_last_error(void);
 int lv_version(void);
+/* number of kernels this library has launched in the process (evidence counter) */
+long long lv_kernel_launches(void);
 
 int lv_index_create(const lv_index_desc *desc, int device, lv_index **out);
 void lv_index_destroy(lv_index *index);

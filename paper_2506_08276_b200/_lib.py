@@ -74,6 +74,7 @@ class EncoderStats(C.Structure):
 EXPORTS = {
     "lv_last_error": (C.c_char_p, []),
     "lv_version": (C.c_int, []),
+    "lv_kernel_launches": (C.c_longlong, []),
     "lv_index_create": (C.c_int, [C.POINTER(IndexDesc), C.c_int, C.POINTER(C.c_void_p)]),
     "lv_index_destroy": (None, [C.c_void_p]),
     "lv_index_set_matrix": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),

@@ -7,6 +7,7 @@
 // a host loop alternating frontier launches with one packed encoder forward
 // over every in-flight query's recompute request (dynamic batching).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -21,6 +22,8 @@ namespace lv {
 
 static thread_local std::string g_last_error;
 void set_error(const std::string &msg) { g_last_error = msg; }
+static std::atomic<long long> g_launches{0};
+void note_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 template <typename T>
 static int dalloc(T **p, size_t count) {
@@ -64,6 +67,7 @@ struct Workspace {
   DBuf<uint32_t> abits, xbits;
   DBuf<int32_t> xlist, req, greq;
   DBuf<int32_t> counters;  // [0] greq_total, [1] queue_head, [2] done_count
+  DBuf<unsigned long long> bytes;  // frontier algorithmic bytes
   DBuf<float> emb;
   DBuf<float> luts;
   DBuf<float> q, qn;
@@ -152,6 +156,7 @@ extern "C" {
 
 const char *lv_last_error(void) { return g_last_error.c_str(); }
 int lv_version(void) { return 1; }
+long long lv_kernel_launches(void) { return g_launches.load(); }
 
 int lv_index_create(const lv_index_desc *d, int device, lv_index **out) {
   LV_REQUIRE(d && out, LV_ERR_USAGE, "lv_index_create: null argument");
@@ -369,6 +374,8 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   LV_TRY(ws.xlist.ensure((size_t)slots * xl_cap));
   LV_TRY(ws.req.ensure((size_t)slots * req_cap));
   LV_TRY(ws.counters.ensure(4));
+  LV_TRY(ws.bytes.ensure(1));
+  LV_CHECK_CUDA(cudaMemsetAsync(ws.bytes.ptr, 0, 8, s));
   const int greq_cap = enc_src ? slots * req_cap : 0;
   if (enc_src) {
     LV_TRY(ws.greq.ensure(greq_cap));
@@ -429,6 +436,7 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   c.greq_cap = greq_cap;
   c.queue_head = ws.counters.ptr + 1;
   c.done_count = ws.counters.ptr + 2;
+  c.bytes_total = ws.bytes.ptr;
   c.out_ids = d_ids;
   c.out_dist = d_dist;
   c.out_count = d_count;
@@ -483,6 +491,10 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  unsigned long long bytes = 0;
+  LV_CHECK_CUDA(cudaMemcpyAsync(&bytes, ws.bytes.ptr, 8, cudaMemcpyDeviceToHost, s));
+  LV_CHECK_CUDA(cudaStreamSynchronize(s));
+  ix->stats.adc_bytes += (int64_t)bytes;
   ix->stats.iterations += iterations;
   ix->stats.physical_encodes += physical;
   ix->stats.frontier_ms += frontier_ms;
@@ -621,7 +633,9 @@ extern "C" int lv_search_batch(lv_index *ix, const float *q, const float *qnorm,
     LV_CHECK_CUDA(cudaMemcpyAsync(ridx.ptr, redo.data(), R * 4, cudaMemcpyHostToDevice, s));
     gather_rows_kernel<<<(unsigned)(((int64_t)R * ix->dim + 255) / 256), 256, 0, s>>>(
         d_q, ridx.ptr, R, ix->dim, rq.ptr);
+        note_launch();
     gather_rows_kernel<<<(R + 255) / 256, 256, 0, s>>>(d_qn, ridx.ptr, R, 1, rqn.ptr);
+    note_launch();
     int32_t *pv = nullptr, *pb = nullptr;
     if (d_visits) {
       LV_TRY(rvis.ensure((size_t)R * out->visits_cap));

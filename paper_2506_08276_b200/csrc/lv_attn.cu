@@ -214,11 +214,13 @@ cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
                              (int)smem);
     if (e != cudaSuccess) return e;
     attn_bf16_kernel<64><<<n_seqs * H, threads, smem, s>>>(qkv, out, S, H, scale_log2);
+    note_launch();
   } else if (dh == 128) {
     e = cudaFuncSetAttribute(attn_bf16_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess) return e;
     attn_bf16_kernel<128><<<n_seqs * H, threads, smem, s>>>(qkv, out, S, H, scale_log2);
+    note_launch();
   } else {
     return cudaErrorInvalidValue;
   }
@@ -236,6 +238,7 @@ cudaError_t attention_f32(const float *qkv, float *out, int n_seqs, int S, int H
   if (e != cudaSuccess) return e;
   attn_f32_kernel<<<(unsigned)((items + warps - 1) / warps), warps * 32, smem, s>>>(
       qkv, out, n_seqs, S, H, dh, 1.0f / sqrtf((float)dh));
+      note_launch();
   return cudaGetLastError();
 }
 

@@ -11,6 +11,8 @@
 namespace lv {
 
 void set_error(const std::string &msg);
+// Process-wide count of kernels this library has launched (lv_kernel_launches).
+void note_launch(long long n = 1);
 
 struct Status {
   int code;

@@ -222,6 +222,7 @@ cudaError_t f32_gemm(const float *A, const float *W, const float *bias, const fl
                      float *out, int M, int N, int K, int epi, cudaStream_t s) {
   dim3 grid((N + 63) / 64, (M + 63) / 64);
   f32_gemm_kernel<<<grid, 256, 0, s>>>(A, W, bias, residual, out, M, N, K, epi);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -369,6 +370,7 @@ int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int
     embed_ln_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, s>>>(
         tokens, token_bytes, S, d_ids, s0, ns, e->tok_emb, e->pos_emb, c.vocab, e->emb_g,
         e->emb_b, d, x);
+        note_launch();
     LV_CHECK_CUDA(cudaGetLastError());
     for (const EncLayer &L : e->layers) {
       LV_TRY(gemm<T>(e, x, L.w_qkv, L.b_qkv, nullptr, qkv, M, 3 * d, d, EPI_BIAS, s));
@@ -380,11 +382,14 @@ int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int
       }
       LV_TRY(gemm<T>(e, ctx, L.w_o, L.b_o, x, y, M, d, d, EPI_BIAS_RESIDUAL, s));
       ln_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, s>>>(y, x, L.ln1_g, L.ln1_b, M, d);
+      note_launch();
       LV_TRY(gemm<T>(e, x, L.w_1, L.b_1, nullptr, h, M, ff, d, EPI_BIAS_GELU, s));
       LV_TRY(gemm<T>(e, h, L.w_2, L.b_2, x, y, M, d, ff, EPI_BIAS_RESIDUAL, s));
       ln_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, s>>>(y, x, L.ln2_g, L.ln2_b, M, d);
+      note_launch();
     }
     pool_kernel<T><<<(unsigned)ns, 256, 0, s>>>(x, out + s0 * d, S, d);
+    note_launch();
     LV_CHECK_CUDA(cudaGetLastError());
   }
   e->passages += n_seqs;

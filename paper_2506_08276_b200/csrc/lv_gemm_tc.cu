@@ -365,6 +365,7 @@ int launch(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
   const int tiles = ((M + kBM - 1) / kBM) * (N / BN);
   const int grid = std::min(tiles, tc_gemm_num_sms());
   tc_gemm_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(ta, tb, M, N, K, bias, residual, out, epi);
+  note_launch();
   LV_CHECK_CUDA(cudaGetLastError());
   return LV_OK;
 }

@@ -263,6 +263,7 @@ __device__ void compute_request_distances(const SearchCtx &c, const SlotPtrs &P,
 // Exact results of a request flow back into the traversal state.
 __device__ void resolve(const SearchCtx &c, const SlotPtrs &P, SlotState &S, const WarpSmem &W) {
   compute_request_distances(c, P, S, W);
+  S.bytes += 4 * (long long)c.dim * S.req_n;
   const int lane = lane_id();
   if (S.phase == PH_ENTRY) {
     float d0 = W.req_d[0];
@@ -328,6 +329,7 @@ __device__ void finish_query(const SearchCtx &c, const SlotPtrs &P, SlotState &S
     c.out_dist[qo + j] = 0.f;
   }
   if (lane == 0) {
+    if (c.bytes_total) atomicAdd(c.bytes_total, (unsigned long long)S.bytes);
     c.out_count[S.qi] = cnt;
     c.out_counters[(int64_t)S.qi * 4 + 0] = S.recomps;
     c.out_counters[(int64_t)S.qi * 4 + 1] = S.approx;
@@ -410,6 +412,7 @@ __device__ void adc_insert(const SearchCtx &c, const SlotPtrs &P, SlotState &S,
   for (int j = lane; j < s0; j += 32) P.aq[j] = W.newk[j];
   __syncwarp();
   S.aq_len = L + F;
+  S.bytes += (long long)c.m * F;
   S.n_elig += n_el;
   S.approx += F;
 }
@@ -462,6 +465,7 @@ __device__ bool advance(const SearchCtx &c, const SlotPtrs &P, SlotState &S, con
         continue;
       }
       int cnt = filter_row(c, S.cur, S.level, P.xbits, P.req);
+      S.bytes += 16 + 4 * (long long)(c.offs[S.level][S.cur + 1] - c.offs[S.level][S.cur]);
       if (cnt == 0) {
         S.level -= 1;
         continue;
@@ -480,6 +484,7 @@ __device__ bool advance(const SearchCtx &c, const SlotPtrs &P, SlotState &S, con
       c.visits[(int64_t)S.qi * c.visits_cap + S.visits_n] = u;
     S.visits_n += 1;
     S.expansions += 1;
+    S.bytes += 16 + 4 * (long long)(c.offs[0][u + 1] - c.offs[0][u]);
     if (c.mode == LV_MODE_EXACT_BESTFIRST) {
       int cnt = filter_row(c, u, 0, P.xbits, P.req);
       if (cnt == 0) continue;
@@ -515,6 +520,7 @@ __device__ bool claim(const SearchCtx &c, SlotState &S) {
   S.phase = PH_ENTRY;
   S.level = c.level_count - 1;
   S.status = LV_Q_OK;
+  if (c.mode == LV_MODE_TWO_LEVEL) S.bytes = 4LL * c.m * kCentroids;  // the query's LUT
   return true;
 }
 
@@ -668,17 +674,20 @@ cudaError_t launch_frontier(const SearchCtx &ctx, cudaStream_t s) {
   }
   int blocks = (ctx.slots + kWarpsPerBlock - 1) / kWarpsPerBlock;
   frontier_kernel<<<blocks, kWarpsPerBlock * 32, smem, s>>>(ctx);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_qnorm(const float *q, int B, int dim, float *qn, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   qnorm_kernel<<<(B + 127) / 128, 128, 0, s>>>(q, B, dim, qn);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_slot_reset(SlotState *st, int slots, cudaStream_t s) {
   slot_reset_kernel<<<(slots + 255) / 256, 256, 0, s>>>(st, slots);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -686,6 +695,7 @@ cudaError_t launch_lut(const float *q, const float *qn, int B, int dim, int metr
                        const float *codebooks, int m, int padded, float *luts, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   lut_kernel<<<B, 256, padded * sizeof(float), s>>>(q, qn, dim, metric, codebooks, m, padded, luts);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -693,6 +703,7 @@ cudaError_t launch_adc_score(const float *lut, int m, const uint8_t *codes, cons
                              int64_t count, float *out, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   adc_score_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(lut, m, codes, ids, count, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -701,6 +712,7 @@ cudaError_t launch_distance_many(int metric, const float *rows, int64_t nrows, i
   if (nrows <= 0) return cudaSuccess;
   int64_t threads = nrows * 4;
   dist_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(metric, rows, nrows, dim, q, qn, out);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -31,6 +31,7 @@ struct SlotState {
   long long approx;
   long long hits;
   long long expansions;
+  long long bytes;   // algorithmic HBM bytes of this query's traversal
 };
 
 struct SearchCtx {
@@ -75,6 +76,7 @@ struct SearchCtx {
   int32_t greq_cap;
   int32_t *queue_head;
   int32_t *done_count;
+  unsigned long long *bytes_total;  // summed SlotState::bytes of finished queries
   // outputs
   int64_t *out_ids;
   float *out_dist;
