@@ -388,6 +388,7 @@ def main():
     sampler.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")
     ev0.record(stream)
     all_ids, all_idx, recomputes, physical, frontier_ms, enc_ms, adc_bytes, iters = \
         [], [], 0, 0, 0.0, 0.0, 0, 0
@@ -409,6 +410,7 @@ def main():
         all_ids.append(ids.cpu().numpy())
         all_idx.append(idx)
     ev1.record(stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     barrier()
     clocks = sampler.stop()
@@ -490,7 +492,7 @@ def main():
         "value": round(qps, 3), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (uniform tokens, random-init encoder weights, PCG64 seeds)",
+        "data": f"synthetic ({W['corpus']} tokens, random-init encoder weights, PCG64 seeds)",
         "config": {"workload": cfg["workload"], "queries_per_rank_per_step": batch,
                    "global_batch": batch * world, "seq_len": cfg["seq"], "ef": ef,
                    "rerank_percent": args.alpha, "parallelism": f"dp{world} (query shards)",
