@@ -66,6 +66,9 @@ extern "C" {
 #define LV_SOURCE_ENCODER 1  /* recompute with the attached encoder (ProviderSource) */
 
 #define LV_IO_DEVICE 1       /* pointer arguments are device pointers */
+#define LV_NO_SHARED_RECOMPUTE 2  /* lv_search_params.flags: encode every request, even
+                                     when another in-flight query recomputed the node
+                                     earlier in the same call (results are identical) */
 
 /* per-query status codes written to lv_search_outputs.status */
 #define LV_Q_OK 0

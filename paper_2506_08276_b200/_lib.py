@@ -18,6 +18,7 @@ LV_MODE = {"exact_bestfirst": 0, "two_level": 1}
 LV_SOURCE_MATRIX = 0
 LV_SOURCE_ENCODER = 1
 LV_IO_DEVICE = 1
+LV_NO_SHARED_RECOMPUTE = 2
 
 
 class IndexDesc(C.Structure):

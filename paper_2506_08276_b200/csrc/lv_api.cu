@@ -69,6 +69,7 @@ struct Workspace {
   DBuf<int32_t> counters;  // [0] greq_total, [1] queue_head, [2] done_count
   DBuf<unsigned long long> bytes;  // frontier algorithmic bytes
   DBuf<float> emb;
+  DBuf<int32_t> hkeys, hvals, new_ids, emb_map, row_count;  // shared-recompute table
   DBuf<float> luts;
   DBuf<float> q, qn;
   DBuf<int64_t> out_ids, out_counters;
@@ -377,16 +378,32 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   LV_TRY(ws.bytes.ensure(1));
   LV_CHECK_CUDA(cudaMemsetAsync(ws.bytes.ptr, 0, 8, s));
   const int greq_cap = enc_src ? slots * req_cap : 0;
+  const bool shared = enc_src && !(p.flags & LV_NO_SHARED_RECOMPUTE);
+  int64_t tab_rows = greq_cap;
+  uint32_t hmask = 0;
   if (enc_src) {
     LV_TRY(ws.greq.ensure(greq_cap));
-    LV_TRY(ws.emb.ensure((size_t)greq_cap * ix->dim));
+    if (shared) {
+      // step-wide table of recomputed rows: <= 8 GiB, at least 4 iterations' worth
+      const int64_t budget = ((int64_t)8 << 30) / ((int64_t)ix->dim * 4);
+      tab_rows = std::max<int64_t>(greq_cap, std::min<int64_t>(budget, 16LL * greq_cap));
+      uint64_t hs = 1;
+      while (hs < (uint64_t)(2 * tab_rows)) hs <<= 1;
+      hmask = (uint32_t)(hs - 1);
+      LV_TRY(ws.hkeys.ensure(hs));
+      LV_TRY(ws.hvals.ensure(hs));
+      LV_TRY(ws.new_ids.ensure(greq_cap));
+      LV_TRY(ws.emb_map.ensure(greq_cap));
+      LV_TRY(ws.row_count.ensure(1));
+    }
+    LV_TRY(ws.emb.ensure((size_t)tab_rows * ix->dim));
   }
   if (two_level) {
     LV_TRY(ws.luts.ensure((size_t)B * ix->m * kCentroids));
     LV_CHECK_CUDA(launch_lut(d_q, d_qn, B, ix->dim, ix->metric, ix->codebooks, ix->m, ix->padded,
                              ws.luts.ptr, s));
   }
-  if (!ws.h_counters) LV_CHECK_CUDA(cudaMallocHost(&ws.h_counters, 16));
+  if (!ws.h_counters) LV_CHECK_CUDA(cudaMallocHost(&ws.h_counters, 32));
   LV_CHECK_CUDA(launch_slot_reset(ws.st.ptr, slots, s));
   LV_CHECK_CUDA(cudaMemsetAsync(ws.counters.ptr, 0, 16, s));
 
@@ -411,6 +428,7 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   c.source = p.source;
   c.matrix = ix->matrix;
   c.emb_buf = ws.emb.ptr;
+  c.emb_map = shared ? ws.emb_map.ptr : nullptr;
   c.B = B;
   c.q = d_q;
   c.qn = d_qn;
@@ -462,6 +480,15 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   } else {
     LV_REQUIRE(ix->enc && ix->tokens, LV_ERR_USAGE,
                "encoder source requires lv_index_attach_encoder");
+    int32_t row_base = 0;
+    auto reset_table = [&]() -> int {
+      LV_CHECK_CUDA(cudaMemsetAsync(ws.hkeys.ptr, 0xff, ((size_t)hmask + 1) * 4, s));
+      LV_CHECK_CUDA(cudaMemsetAsync(ws.hvals.ptr, 0xff, ((size_t)hmask + 1) * 4, s));
+      LV_CHECK_CUDA(cudaMemsetAsync(ws.row_count.ptr, 0, 4, s));
+      row_base = 0;
+      return LV_OK;
+    };
+    if (shared) LV_TRY(reset_table());
     while (true) {
       LV_CHECK_CUDA(cudaMemsetAsync(ws.counters.ptr, 0, 4, s));  // greq_total
       cudaEventRecord(e0, s);
@@ -475,14 +502,32 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
       ++iterations;
       const int total = ws.h_counters[0];
       if (total > 0) {
+        const int32_t *enc_ids = ws.greq.ptr;
+        int32_t n_new = total;
+        float *enc_out = ws.emb.ptr;
+        if (shared) {
+          // one encode per distinct node of the step; repeats reuse its row
+          if ((int64_t)row_base + total > tab_rows) LV_TRY(reset_table());
+          LV_CHECK_CUDA(launch_dedup(ws.greq.ptr, total, ws.hkeys.ptr, ws.hvals.ptr, hmask,
+                                     ws.row_count.ptr, row_base, ws.new_ids.ptr, ws.emb_map.ptr,
+                                     s));
+          LV_CHECK_CUDA(cudaMemcpyAsync(ws.h_counters + 3, ws.row_count.ptr, 4,
+                                        cudaMemcpyDeviceToHost, s));
+          LV_CHECK_CUDA(cudaStreamSynchronize(s));
+          n_new = ws.h_counters[3] - row_base;
+          enc_ids = ws.new_ids.ptr;
+          enc_out = ws.emb.ptr + (size_t)row_base * ix->dim;
+          row_base = ws.h_counters[3];
+        }
         cudaEventRecord(e0, s);
-        LV_TRY(encode_node_rows(ix->enc, ix->tokens, ix->token_bytes, ix->seq_len, ws.greq.ptr,
-                                total, ws.emb.ptr, s));
+        if (n_new > 0)
+          LV_TRY(encode_node_rows(ix->enc, ix->tokens, ix->token_bytes, ix->seq_len, enc_ids,
+                                  n_new, enc_out, s));
         cudaEventRecord(e1, s);
         LV_CHECK_CUDA(cudaEventSynchronize(e1));
         cudaEventElapsedTime(&ms, e0, e1);
         encoder_ms += ms;
-        physical += total;
+        physical += n_new;
       } else if (ws.h_counters[2] >= B) {
         break;
       }

@@ -131,6 +131,89 @@ __global__ void ln_kernel(const T *__restrict__ in, T *__restrict__ out, const f
     }
 }
 
+// bf16 LayerNorm with 16-byte accesses (d % 256 == 0): lane owns chunks
+// i*32 + lane of 8 elements; HBM-bound, one warp per row.
+template <int NV>
+__global__ void ln_bf16_vec_kernel(const __nv_bfloat16 *__restrict__ in,
+                                   __nv_bfloat16 *__restrict__ out, const float *__restrict__ g,
+                                   const float *__restrict__ b, int64_t rows) {
+  constexpr int d = NV * 256;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const uint4 *x = reinterpret_cast<const uint4 *>(in + row * d);
+  float v[NV][8];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    uint4 u = __ldg(x + i * 32 + lane);
+    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(h[e]);
+      v[i][2 * e] = f.x;
+      v[i][2 * e + 1] = f.y;
+      s += f.x + f.y;
+    }
+  }
+  const float mean = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float t = v[i][e] - mean;
+      q += t * t;
+    }
+  const float rstd = rsqrtf(warp_sum(q) / d + kLnEps);
+  uint4 *o = reinterpret_cast<uint4 *>(out + row * d);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c0 = (i * 32 + lane) * 8;
+    const float4 g0 = __ldg(reinterpret_cast<const float4 *>(g + c0));
+    const float4 g1 = __ldg(reinterpret_cast<const float4 *>(g + c0 + 4));
+    const float4 b0 = __ldg(reinterpret_cast<const float4 *>(b + c0));
+    const float4 b1 = __ldg(reinterpret_cast<const float4 *>(b + c0 + 4));
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    uint4 u;
+    uint32_t *w = reinterpret_cast<uint32_t *>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 h = __floats2bfloat162_rn((v[i][2 * e] - mean) * rstd * gg[2 * e] + bb[2 * e],
+                                               (v[i][2 * e + 1] - mean) * rstd * gg[2 * e + 1] +
+                                                   bb[2 * e + 1]);
+      w[e] = *reinterpret_cast<uint32_t *>(&h);
+    }
+    o[i * 32 + lane] = u;
+  }
+}
+
+template <typename T>
+void launch_ln(const T *in, T *out, const float *g, const float *b, int64_t rows, int d,
+               cudaStream_t s) {
+  const unsigned blocks = (unsigned)((rows + 7) / 8);
+  if constexpr (sizeof(T) == 2) {
+    if (d == 256) {
+      ln_bf16_vec_kernel<1><<<blocks, 256, 0, s>>>(in, out, g, b, rows);
+      note_launch();
+      return;
+    }
+    if (d == 768) {
+      ln_bf16_vec_kernel<3><<<blocks, 256, 0, s>>>(in, out, g, b, rows);
+      note_launch();
+      return;
+    }
+    if (d == 1024) {
+      ln_bf16_vec_kernel<4><<<blocks, 256, 0, s>>>(in, out, g, b, rows);
+      note_launch();
+      return;
+    }
+  }
+  ln_kernel<T><<<blocks, 256, 0, s>>>(in, out, g, b, rows, d);
+  note_launch();
+}
+
 // Mean over the S token rows of each sequence, then L2 normalisation
 // (x / max(||x||, 1e-12)). One block per sequence, fixed summation order.
 template <typename T>
@@ -381,12 +464,10 @@ int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int
         LV_CHECK_CUDA(attention_f32((const float *)qkv, (float *)ctx, (int)ns, S, H, dh, s));
       }
       LV_TRY(gemm<T>(e, ctx, L.w_o, L.b_o, x, y, M, d, d, EPI_BIAS_RESIDUAL, s));
-      ln_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, s>>>(y, x, L.ln1_g, L.ln1_b, M, d);
-      note_launch();
+      launch_ln<T>(y, x, L.ln1_g, L.ln1_b, M, d, s);
       LV_TRY(gemm<T>(e, x, L.w_1, L.b_1, nullptr, h, M, ff, d, EPI_BIAS_GELU, s));
       LV_TRY(gemm<T>(e, h, L.w_2, L.b_2, x, y, M, d, ff, EPI_BIAS_RESIDUAL, s));
-      ln_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, s>>>(y, x, L.ln2_g, L.ln2_b, M, d);
-      note_launch();
+      launch_ln<T>(y, x, L.ln2_g, L.ln2_b, M, d, s);
     }
     pool_kernel<T><<<(unsigned)ns, 256, 0, s>>>(x, out + s0 * d, S, d);
     note_launch();

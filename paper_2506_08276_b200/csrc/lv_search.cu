@@ -238,7 +238,7 @@ __device__ void compute_request_distances(const SearchCtx &c, const SlotPtrs &P,
       } else {
         int mi = W.miss_idx[r];
         row = (mi < 0) ? c.cache_rows + (int64_t)c.cache_slot[w] * c.dim
-                       : c.emb_buf + (int64_t)(S.req_off + mi) * c.dim;
+              : c.emb_buf + (int64_t)(c.emb_map ? c.emb_map[S.req_off + mi] : S.req_off + mi) * c.dim;
       }
       if (c.metric == LV_METRIC_L2) {
         a_dot = einsum_lane<true>(row, qv, c.dim, l);
@@ -642,6 +642,43 @@ __global__ void dist_kernel(int metric, const float *__restrict__ rows, int64_t 
     out[r] = finish_distance(metric, einsum_combine(a0, a1, a2, a3), einsum_combine(b0, b1, b2, b3), qn);
 }
 
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__global__ void dedup_kernel(const int32_t *__restrict__ greq, int total, int32_t *keys,
+                             int32_t *vals, uint32_t mask, int32_t *row_count, int32_t base,
+                             int32_t *__restrict__ new_ids, int32_t *__restrict__ map) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= total) return;
+  const int32_t w = greq[r];
+  uint32_t slot = mix32((uint32_t)w) & mask;
+  while (true) {
+    const int32_t k = atomicCAS(keys + slot, -1, w);
+    if (k == -1) {  // first request of w in this step: claim a row, schedule its encode
+      const int32_t row = atomicAdd(row_count, 1);
+      new_ids[row - base] = w;
+      atomicExch(vals + slot, row);
+      map[r] = row;
+      return;
+    }
+    if (k == w) {  // shared: wait for the claimer to publish the row
+      int32_t row;
+      do {
+        row = atomicAdd(vals + slot, 0);
+      } while (row < 0);
+      map[r] = row;
+      return;
+    }
+    slot = (slot + 1) & mask;
+  }
+}
+
 __global__ void qnorm_kernel(const float *__restrict__ q, int B, int dim, float *__restrict__ qn) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B) return;
@@ -674,6 +711,16 @@ cudaError_t launch_frontier(const SearchCtx &ctx, cudaStream_t s) {
   }
   int blocks = (ctx.slots + kWarpsPerBlock - 1) / kWarpsPerBlock;
   frontier_kernel<<<blocks, kWarpsPerBlock * 32, smem, s>>>(ctx);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dedup(const int32_t *greq, int total, int32_t *keys, int32_t *vals,
+                         uint32_t mask, int32_t *row_count, int32_t base, int32_t *new_ids,
+                         int32_t *map, cudaStream_t s) {
+  if (total <= 0) return cudaSuccess;
+  dedup_kernel<<<(total + 255) / 256, 256, 0, s>>>(greq, total, keys, vals, mask, row_count, base,
+                                                   new_ids, map);
   note_launch();
   return cudaGetLastError();
 }

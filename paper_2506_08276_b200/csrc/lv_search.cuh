@@ -52,7 +52,8 @@ struct SearchCtx {
   // exact-vector source
   int32_t source;
   const float *matrix;   // [n][dim]  (LV_SOURCE_MATRIX)
-  const float *emb_buf;  // [greq_cap][dim]  (LV_SOURCE_ENCODER)
+  const float *emb_buf;  // recomputed rows (LV_SOURCE_ENCODER)
+  const int32_t *emb_map;  // request index -> row of emb_buf (shared-recompute table), or null
   // queries
   int32_t B;
   const float *q;   // [B][dim]
@@ -101,6 +102,13 @@ cudaError_t launch_adc_score(const float *lut, int m, const uint8_t *codes, cons
                              int64_t count, float *out, cudaStream_t s);
 cudaError_t launch_distance_many(int metric, const float *rows, int64_t nrows, int dim,
                                  const float *q, float qn, float *out, cudaStream_t s);
+// Shared recomputation (cross-query dedup): map each of the `total` requested
+// node ids to a row of the step's embedding table, claiming new rows for ids
+// not seen before in this step (their ids are appended to new_ids at
+// row - *base). keys/vals: open-addressing table of `mask + 1` slots.
+cudaError_t launch_dedup(const int32_t *greq, int total, int32_t *keys, int32_t *vals,
+                         uint32_t mask, int32_t *row_count, int32_t base, int32_t *new_ids,
+                         int32_t *map, cudaStream_t s);
 cudaError_t launch_qnorm(const float *q, int B, int dim, float *qn, cudaStream_t s);
 cudaError_t launch_slot_reset(SlotState *st, int slots, cudaStream_t s);
 cudaError_t launch_frontier(const SearchCtx &ctx, cudaStream_t s);

@@ -274,7 +274,8 @@ class DeviceIndex:
     # -- search
     def search(self, Q, params: SearchParams, source, qn=None,
                cache: EmbeddingCache | None = None, trace: bool = False,
-               max_inflight: int = 0, stream=None) -> list[SearchReport]:
+               max_inflight: int = 0, stream=None,
+               shared_recompute: bool = True) -> list[SearchReport]:
         """Run ``len(Q)`` queries concurrently; one ``SearchReport`` per query."""
         t0 = time.perf_counter()
         Q = np.ascontiguousarray(Q, dtype=np.float32)
@@ -290,6 +291,7 @@ class DeviceIndex:
         p.batch_size = params.batch_size
         p.mode = _lib.LV_MODE[params.mode]
         p.max_inflight = max_inflight
+        p.flags = 0 if shared_recompute else _lib.LV_NO_SHARED_RECOMPUTE
         if isinstance(source, MatrixSource):
             p.source = _lib.LV_SOURCE_MATRIX
             self.set_matrix(source.matrix)
@@ -351,7 +353,7 @@ class DeviceIndex:
 
     def search_device(self, Q, params: SearchParams, source, qn=None,
                       cache: EmbeddingCache | None = None, max_inflight: int = 0,
-                      out: dict | None = None):
+                      out: dict | None = None, shared_recompute: bool = True):
         """Device-resident batch search: ``Q`` is a CUDA float32 tensor [B, dim],
         ``qn`` a CUDA tensor [B] or None (norms then computed on the device).
         Returns CUDA tensors ids [B, k] (int64, -1 padded), dist [B, k],
@@ -369,7 +371,7 @@ class DeviceIndex:
         p.batch_size = params.batch_size
         p.mode = _lib.LV_MODE[params.mode]
         p.max_inflight = max_inflight
-        p.flags = _lib.LV_IO_DEVICE
+        p.flags = _lib.LV_IO_DEVICE | (0 if shared_recompute else _lib.LV_NO_SHARED_RECOMPUTE)
         if isinstance(source, MatrixSource):
             p.source = _lib.LV_SOURCE_MATRIX
             self.set_matrix(source.matrix)

@@ -131,3 +131,28 @@ def test_device_io_search_and_device_qnorm(world):
     torch.cuda.synchronize()
     same = (out2["ids"].cpu().numpy() == ids).all(1).mean()
     assert same >= 0.95
+
+
+def test_shared_recompute_is_transparent(world):
+    """Sharing recomputations across in-flight queries changes only the physical
+    encode count: ids, distance bits and the per-query (logical) counters are
+    those of the unshared run."""
+    lv = world["lv"]
+    from paper_2506_08276_b200.encoder import EncoderProvider
+    w = world["bf16"]
+    g = lv.load_graph(w["dir"] / "graph.bin")
+    model, codes = lv.load_pq(w["dir"] / "pq.bin")
+    params = lv.SearchParams(k=3, ef=32, rerank_percent=30.0)
+    qn = lv.search.query_norms(w["Q"])
+    dev = lv.search.device_index_for(g, model, codes)
+    src = lv.ProviderSource(EncoderProvider(w["enc"], w["store"]))
+    a = dev.search(w["Q"], params, src, qn=qn, shared_recompute=False)
+    phys_a = dev.last_stats()["physical_encodes"]
+    b = dev.search(w["Q"], params, src, qn=qn, shared_recompute=True)
+    phys_b = dev.last_stats()["physical_encodes"]
+    for x, y in zip(a, b):
+        assert x.results == y.results
+        assert x.recomputations == y.recomputations
+        assert x.approx_lookups == y.approx_lookups
+    assert phys_a == sum(x.recomputations for x in a)
+    assert phys_b < phys_a
