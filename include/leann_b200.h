@@ -189,6 +189,9 @@ int lv_encoder_reset_stats(lv_encoder *enc);
  * epi: 0 bias, 1 bias + erf-GELU, 2 bias + residual. N % 128 == 0, K % 64 == 0. */
 int lv_gemm_bf16(const void *A, const void *W, const float *bias, const void *residual,
                  void *out, int32_t M, int32_t N, int32_t K, int32_t epi, void *stream);
+/* GEMM kernel selection: 0 = auto (2-CTA cta_group::2 kernel when N % 256 == 0),
+ * 1 = 1-CTA kernel only. Returns the previous mode. */
+int lv_set_gemm_mode(int mode);
 
 #ifdef __cplusplus
 }

@@ -631,6 +631,12 @@ int lv_gemm_bf16(const void *A, const void *W, const float *bias, const void *re
                  (cudaStream_t)stream);
 }
 
+int lv_set_gemm_mode(int mode) {
+  const int prev = g_gemm_mode;
+  g_gemm_mode = mode;
+  return prev;
+}
+
 int lv_encoder_profile(lv_encoder *enc, int enable) {
   LV_REQUIRE(enc, LV_ERR_USAGE, "null encoder");
   enc->profile = enable != 0;

@@ -24,6 +24,7 @@ int tc_gemm(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
             const __nv_bfloat16 *residual, __nv_bfloat16 *out, int M, int N, int K, int epi,
             cudaStream_t s);
 int tc_gemm_num_sms();
+extern int g_gemm_mode;  // 0 auto (2-CTA pair kernel when N % 256 == 0), 1 force 1-CTA
 
 // ---- fp32 SIMT GEMM (parity mode, lv_encoder.cu): same contract in fp32.
 cudaError_t f32_gemm(const float *A, const float *W, const float *bias, const float *residual,

@@ -21,13 +21,17 @@ def _torch():
     return torch
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("M,N,K,epi", [
     (128, 256, 64, 0), (1000, 768, 768, 0), (777, 2304, 768, 0), (640, 3072, 768, 1),
     (513, 768, 3072, 2), (300, 128, 256, 2), (4096, 1024, 256, 1), (129, 384, 512, 0),
+    (100000, 2304, 768, 0), (70000, 768, 3072, 2),
 ])
-def test_tc_gemm_matches_torch(lv, M, N, K, epi):
+def test_tc_gemm_matches_torch(lv, M, N, K, epi, mode):
+    """mode 0: 2-CTA (cta_group::2) kernel where N % 256 == 0; mode 1: 1-CTA kernel."""
     torch = _torch()
     from paper_2506_08276_b200 import _lib
+    _lib.lib().lv_set_gemm_mode(mode)
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
     A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
@@ -43,6 +47,7 @@ def test_tc_gemm_matches_torch(lv, M, N, K, epi):
         ref = torch.nn.functional.gelu(ref)
     elif epi == 2:
         ref = ref + res.float()
+    _lib.lib().lv_set_gemm_mode(0)
     err = (out.float() - ref).abs()
     tol = 2e-2 * ref.abs() + 2e-2  # bf16 output rounding (2^-8 relative) + fp32 order
     assert bool((err <= tol).all()), float(err.max())
