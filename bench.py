@@ -345,10 +345,11 @@ def main():
     source = lv.ProviderSource(prov)
     nq = cfg["n_queries"]
 
+    from paper_2506_08276_b200.dist import (gather_results, max_over_ranks, shard_queries,
+                                            sum_over_ranks)
+
     def query_slice(step):
-        start = ((step * world + rank) * batch) % nq
-        idx = (np.arange(batch) + start) % nq
-        return idx
+        return shard_queries(step, rank, world, batch, nq)
 
     slices = {}
     out_buf = {}
@@ -403,10 +404,7 @@ def main():
         recomputes += int(out["counters"][:batch, 0].sum().item())
         ids = out["ids"][:batch]
         if dist is not None:  # the one collective: gather result ids/scores
-            g_ids = torch.empty((world * batch, k), dtype=ids.dtype, device=ids.device)
-            dist.all_gather_into_tensor(g_ids, ids.contiguous())
-            g_d = torch.empty((world * batch, k), dtype=torch.float32, device=ids.device)
-            dist.all_gather_into_tensor(g_d, out["dist"][:batch].contiguous())
+            gather_results(ids, out["dist"][:batch])
         all_ids.append(ids.cpu().numpy())
         all_idx.append(idx)
     ev1.record(stream)
@@ -418,15 +416,9 @@ def main():
     launches = _lib.lib().lv_kernel_launches() - launches0
     est = W["enc"].stats()
     W["enc"].profile(False)
-    if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        agg = torch.tensor([recomputes, physical, launches], dtype=torch.float64, device="cuda")
-        dist.all_reduce(agg)
-        recomputes_all, physical_all, launches_all = (int(x) for x in agg.tolist())
-    else:
-        recomputes_all, physical_all, launches_all = recomputes, physical, launches
+    ms = max_over_ranks(ms, device="cuda")
+    recomputes_all, physical_all, launches_all = (
+        int(x) for x in sum_over_ranks([recomputes, physical, launches], device="cuda"))
     secs = ms / 1000.0
     total_q = batch * args.steps * world
     ids_np = np.concatenate(all_ids)
@@ -461,10 +453,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ems = e0.elapsed_time(e1)
-        if dist is not None:
-            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(ems, device="cuda")
         e2e = {"value": total_q / (ems / 1000.0), "unit": "queries/s",
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
 
