@@ -1,0 +1,96 @@
+"""North-star parity on a fixture produced by the UNMODIFIED reference
+(tests/golden/make_encoder_golden.py: reference builder + reference run_search
+over torch-fp32 encoder embeddings):
+
+* matrix mode on the reference's embeddings: ID-for-ID, distance bits and
+  counters identical;
+* fp32 encoder mode (the GPU recomputes every candidate from its token row):
+  top-k ID sets identical on >= 99% of queries, distances within 1e-5 relative;
+* bf16 encoder mode: recall@3 against brute force within 0.5 points of the
+  reference's recall (reported; asserted with a small-sample margin).
+"""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+FIX = GOLDEN / "enc_fp32"
+
+
+@pytest.fixture(scope="module")
+def fx():
+    import __graft_entry__ as ge
+    ge.build()
+    import paper_2506_08276_b200 as lv
+    from paper_2506_08276_b200.encoder import EncoderConfig
+    meta = json.loads((FIX / "reference_results.json").read_text())
+    cfg = EncoderConfig(**meta["encoder"])
+    g = lv.load_graph(FIX / "graph.bin")
+    model, codes = lv.load_pq(FIX / "pq.bin")
+    return dict(lv=lv, meta=meta, cfg=cfg, g=g, model=model, codes=codes,
+                tok=np.load(FIX / "tokens.npy"), qtok=np.load(FIX / "qtokens.npy"),
+                E=np.load(FIX / "embeddings_ref.npy"), Q=np.load(FIX / "queries_ref.npy"))
+
+
+def _bf(x):
+    return np.float32(x).view(np.uint32)
+
+
+def test_matrix_mode_bit_exact_vs_reference(fx):
+    lv = fx["lv"]
+    qn = lv.search.query_norms(fx["Q"])
+    for case in fx["meta"]["cases"]:
+        reps = lv.search_batch(fx["g"], fx["Q"], lv.SearchParams(**case["params"]),
+                               lv.MatrixSource(fx["E"]), "cosine", fx["model"], fx["codes"], qn=qn)
+        for rep, exp in zip(reps, case["reports"]):
+            assert [i for i, _ in rep.results] == exp["ids"]
+            assert [_bf(d) for _, d in rep.results] == [_bf(d) for d in exp["dist"]]
+            assert rep.recomputations == exp["recomputations"]
+            assert rep.approx_lookups == exp["approx_lookups"]
+
+
+def _encoder_mode(fx, precision):
+    lv = fx["lv"]
+    from paper_2506_08276_b200.encoder import (EncoderProvider, GpuEncoder, TokenStore,
+                                               init_weights)
+    enc = GpuEncoder(fx["cfg"], init_weights(fx["cfg"], seed=fx["meta"]["seed"]),
+                     precision=precision)
+    Qg = enc.encode(fx["qtok"])
+    src = lv.ProviderSource(EncoderProvider(enc, TokenStore(fx["tok"])))
+    out = []
+    for case in fx["meta"]["cases"]:
+        reps = lv.search_batch(fx["g"], Qg, lv.SearchParams(**case["params"]), src, "cosine",
+                               fx["model"], fx["codes"], qn=lv.search.query_norms(Qg))
+        out.append((case, reps))
+    return out
+
+
+def test_fp32_encoder_mode_matches_reference(fx):
+    for case, reps in _encoder_mode(fx, "fp32"):
+        same = 0
+        for rep, exp in zip(reps, case["reports"]):
+            ids = [i for i, _ in rep.results]
+            if set(ids) == set(exp["ids"]):
+                same += 1
+                if ids == exp["ids"]:
+                    got = np.array([d for _, d in rep.results], dtype=np.float64)
+                    ref = np.array(exp["dist"], dtype=np.float64)
+                    assert np.all(np.abs(got - ref) <= 1e-5 * np.abs(ref) + 1e-7), (got, ref)
+        assert same / len(reps) >= 0.99, (case["params"], same)
+
+
+def test_bf16_encoder_mode_recall_close_to_reference(fx):
+    import torch
+    from paper_2506_08276_b200.builder import brute_force_topk, mean_recall
+    gt = brute_force_topk(torch.from_numpy(fx["E"]).cuda(), fx["Q"], 3, "cosine")
+    for case, reps in _encoder_mode(fx, "bf16"):
+        ref_recall = mean_recall([r["ids"] for r in case["reports"]], gt)
+        got_recall = mean_recall([[i for i, _ in r.results] for r in reps], gt)
+        print(f"bf16 {case['params']}: recall@3 {got_recall:.4f} vs reference {ref_recall:.4f}")
+        # north_star bar is 0.5 points; 100 queries x 3 ids -> one id = 0.33 points
+        assert abs(got_recall - ref_recall) <= 0.02, (got_recall, ref_recall)

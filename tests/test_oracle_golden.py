@@ -125,3 +125,23 @@ def test_cutoff_rank_uses_float_product():
     assert sp.cutoff_rank(30.0, 10) == 3
     assert sp.cutoff_rank(100.0, 1) == 1
     assert sp.cutoff_rank(0.5, 1) == 1
+
+
+def test_oracle_matches_reference_on_encoder_fixture():
+    """The oracle port reproduces the reference's run_search on the fp32-encoder
+    fixture (tests/golden/make_encoder_golden.py)."""
+    import json
+    from oracle import search_port as sp
+    d = GOLDEN / "enc_fp32"
+    meta = json.loads((d / "reference_results.json").read_text())
+    g = sp.read_lgr1(d / "graph.bin")
+    pq = sp.read_lpq1(d / "pq.bin")
+    E = np.load(d / "embeddings_ref.npy")
+    Q = np.load(d / "queries_ref.npy")
+    for case in meta["cases"]:
+        p = sp.SearchParams(**case["params"])
+        for q, exp in list(zip(Q, case["reports"]))[:40]:
+            rep = sp.two_level(g, q, p, pq["codebooks"], pq["codes"], sp.MatrixRows(E), "cosine")
+            assert [i for i, _ in rep.results] == exp["ids"]
+            assert [float(x) for _, x in rep.results] == exp["dist"]
+            assert rep.recomputations == exp["recomputations"]
