@@ -51,7 +51,7 @@ CONFIGS = {
                         "BERT-base (768-d) random-init encoder, high-degree-preserving pruned "
                         "graph (M=32, m=6, beta=2%), PQ m=64, 4096-query pool, top-3",
                n=1_000_000, seq=256, encoder="bert-base", pq_m=64, k=3, n_queries=4096,
-               batch=1024, corpus="lda"),
+               batch=4096, corpus="lda"),
 }
 
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -137,7 +137,8 @@ def setup(cfg, args, device):
     else:
         gen = lambda m, sd: synthetic_tokens(m, cfg["seq"], ecfg.vocab, sd)
     tokens = gen(cfg["n"], args.seed)
-    qtokens = gen(cfg["n_queries"], args.seed + 1)
+    # query pool: the config's queries, extended so every rank serves distinct ones
+    qtokens = gen(max(cfg["n_queries"], args.pool), args.seed + 1)
     weights = init_weights(ecfg, seed=args.seed + 2)
     enc = GpuEncoder(ecfg, weights, precision="bf16", device=device)
     tok_dev = torch.from_numpy(tokens.view(np.int16)).cuda(device)
@@ -180,7 +181,8 @@ def tune(W, cfg, args, dev_index):
     is batch-invariant)."""
     import paper_2506_08276_b200 as lv
     k = cfg["k"]
-    Q = W["Q"]
+    Q = W["Q"][:cfg["n_queries"]].contiguous()   # tune on the config's query set
+    gt_tune = W["gt"][:cfg["n_queries"]]
     table = []
     for alpha in args.alphas:
         memo = {}
@@ -189,7 +191,7 @@ def tune(W, cfg, args, dev_index):
             if ef not in memo:
                 p = lv.SearchParams(k=k, ef=ef, rerank_percent=alpha)
                 out = dev_index.search_device(Q, p, lv.MatrixSource(W["E"]))
-                memo[ef] = (recall_of(out["ids"].cpu().numpy(), W["gt"]),
+                memo[ef] = (recall_of(out["ids"].cpu().numpy(), gt_tune),
                             float(out["counters"][:, 0].double().mean().item()))
                 log(f"tune: alpha={alpha} ef={ef} recall@{k}={memo[ef][0]:.4f} "
                     f"recomputes/q={memo[ef][1]:.0f}")
@@ -282,20 +284,24 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="queries per rank per step")
     ap.add_argument("--ef", type=int, default=0, help="skip tune_ef and use this ef")
     ap.add_argument("--ef-max", type=int, default=512)
-    ap.add_argument("--alphas", default="30,50,100",
+    ap.add_argument("--alphas", default="30,50,70,80,90,100",
                     help="rerank percents tried by the tuner (the first is used with --ef)")
     ap.add_argument("--corpus", default="", choices=["", "lda", "uniform"])
     ap.add_argument("--inflight", type=int, default=0, help="concurrent query slots per rank")
     ap.add_argument("--n", type=int, default=0, help="override the corpus size (profiling only)")
+    ap.add_argument("--cache-percent", type=float, default=2.0,
+                    help="reference EmbeddingCache size (SearchParams.cache_percent)")
     ap.add_argument("--recall", type=float, default=0.90)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    args.pool = 0
     args.alphas = [float(x) for x in args.alphas.split(",")]
     args.alpha = args.alphas[0]
     cfg = dict(CONFIGS[args.config])
+    args.pool = (args.batch or cfg["batch"]) * int(os.environ.get("WORLD_SIZE", "1"))
     if args.n:
         cfg["n"] = args.n
         cfg["workload"] += f" [corpus reduced to n={args.n} for profiling]"
@@ -343,7 +349,14 @@ def main():
 
     prov = EncoderProvider(W["enc"], W["tok_dev"])
     source = lv.ProviderSource(prov)
-    nq = cfg["n_queries"]
+    hub_cache = None
+    if args.cache_percent:
+        # reference EmbeddingCache (search.py:113-142): top-degree nodes' exact
+        # vectors pinned once (untimed setup), results-transparent
+        hub_cache = lv.build_embedding_cache(W["graph"], args.cache_percent)
+        dev_index.attach_encoder(prov)
+        dev_index.set_cache(hub_cache)
+    nq = W["Q"].shape[0]
 
     from paper_2506_08276_b200.dist import (gather_results, max_over_ranks, shard_queries,
                                             sum_over_ranks)
@@ -364,7 +377,7 @@ def main():
             qt = slices[step]
         Qb = W["enc"].encode(qt)
         out = dev_index.search_device(Qb, params, source, qn=None, out=out_buf.get("o"),
-                                      max_inflight=args.inflight)
+                                      max_inflight=args.inflight, cache=hub_cache)
         out_buf["o"] = out
         return idx, out
 
@@ -393,6 +406,7 @@ def main():
     ev0.record(stream)
     all_ids, all_idx, recomputes, physical, frontier_ms, enc_ms, adc_bytes, iters = \
         [], [], 0, 0, 0.0, 0.0, 0, 0
+    cache_hits = 0
     for s in range(args.steps):
         idx, out = step_value(args.warmup + s)
         st = dev_index.last_stats()
@@ -402,6 +416,7 @@ def main():
         adc_bytes += st["adc_bytes"]
         iters += st["iterations"]
         recomputes += int(out["counters"][:batch, 0].sum().item())
+        cache_hits += int(out["counters"][:batch, 2].sum().item())
         ids = out["ids"][:batch]
         if dist is not None:  # the one collective: gather result ids/scores
             gather_results(ids, out["dist"][:batch])
@@ -430,10 +445,11 @@ def main():
     e2e = None
     if not args.no_e2e:
         searcher = LeannSearcher(W["graph"], W["model"], W["codes"], W["enc"], W["tok_dev"],
-                                 rerank_percent=args.alpha)
+                                 rerank_percent=args.alpha, cache_percent=args.cache_percent)
+        e2e_steps = min(args.steps, 2)   # bounds the run time; same step definition
         pinned = [torch.from_numpy(np.ascontiguousarray(
             W["qtokens"][query_slice(args.warmup + s)]).view(np.int16)).pin_memory()
-            for s in range(args.steps)]
+            for s in range(e2e_steps)]
         searcher.search(pinned[0].cuda(), top_k=k, complexity=ef)  # warm
         barrier()
         torch.cuda.synchronize()
@@ -441,7 +457,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         h2d = d2h = 0
-        for s in range(args.steps):
+        for s in range(e2e_steps):
             qt = pinned[s].cuda(non_blocking=True)
             ids, dists, counters = searcher.search(qt, top_k=k, complexity=ef,
                                                    max_inflight=args.inflight)
@@ -454,8 +470,9 @@ def main():
         barrier()
         ems = e0.elapsed_time(e1)
         ems = max_over_ranks(ems, device="cuda")
-        e2e = {"value": total_q / (ems / 1000.0), "unit": "queries/s",
-               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
+        e2e = {"value": batch * e2e_steps * world / (ems / 1000.0), "unit": "queries/s",
+               "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
+               "steps": e2e_steps}
 
     if rank != 0:
         return
@@ -487,12 +504,14 @@ def main():
                    "rerank_percent": args.alpha, "parallelism": f"dp{world} (query shards)",
                    "recall_at_3": round(recall, 4), "tuned_recall_at_3": tuned_recall,
                    "ef_feasible": feasible, "corpus": W["corpus"],
-                   "inflight_slots": args.inflight or min(batch, 4096), "tuning": table, "l2": "inputs larger than L2 (token store "
+                   "inflight_slots": args.inflight or min(batch, 4096), "tuning": table,
+                   "cache_percent": args.cache_percent or None, "l2": "inputs larger than L2 (token store "
                    f"{W['tokens'].nbytes >> 20} MiB, PQ codes {W['codes'].codes.nbytes >> 20} MiB)",
                    "setup_s": round(W["setup_s"], 1)},
         "recomputed_embeddings_per_s": {"logical": round(recomputes_all / secs, 1),
                                         "physical": round(physical_all / secs, 1)},
         "recomputes_per_query": round(recomputes_all / total_q, 2),
+        "cache_hits_per_query": round(cache_hits * world / total_q, 2),
         "encoder_share": round(enc_ms / ms, 4) if ms else None,
         "frontier_iterations": iters,
         "roofline": roofline, "rooflines": rooflines,

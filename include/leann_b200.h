@@ -189,6 +189,10 @@ int lv_encoder_reset_stats(lv_encoder *enc);
  * epi: 0 bias, 1 bias + erf-GELU, 2 bias + residual. N % 128 == 0, K % 64 == 0. */
 int lv_gemm_bf16(const void *A, const void *W, const float *bias, const void *residual,
                  void *out, int32_t M, int32_t N, int32_t K, int32_t epi, void *stream);
+/* Multi-head bidirectional attention of the encoder, bf16 device pointers:
+ * qkv [n_seqs*S][3*H*dh] (q | k | v), out [n_seqs*S][H*dh]. S % 64 == 0, dh in {64, 128}. */
+int lv_attention_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int32_t H,
+                      int32_t dh, void *stream);
 /* GEMM kernel selection: 0 = auto (2-CTA cta_group::2 kernel when N % 256 == 0),
  * 1 = 1-CTA kernel only. Returns the previous mode. */
 int lv_set_gemm_mode(int mode);

@@ -5,9 +5,8 @@
 // head) pair and the whole K/V of that head fits in shared memory.
 //
 //   attention_bf16: flash-style, scores and P.V on tensor cores (mma.sync
-//     m16n8k16 bf16 -> fp32), online softmax in fp32 registers; K row-major
-//     and V transposed in padded shared memory (conflict-free 32-bit fragment
-//     loads). Attention is ~5% of the encoder FLOPs at S <= 512 (the GEMMs in
+//     m16n8k16 bf16 -> fp32, fragments via ldmatrix / ldmatrix.trans), online
+//     softmax in fp32 registers; Q/K/V staged with cp.async. Attention is ~5% of the encoder FLOPs at S <= 512 (the GEMMs in
 //     lv_gemm_tc.cu carry the rest).
 //   attention_f32: parity-mode reference path (one warp per query row, fixed
 //     summation order), used by the fp32 encoder.
@@ -34,49 +33,62 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return *reinterpret_cast<uint32_t *>(&h);
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void *p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void *p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+
+// One CTA per (sequence, head). Q, K, V of the head are staged with 16-byte
+// cp.async into row-major shared memory padded to DH + 8 elements (row stride
+// = 16 * odd bytes, so the 8 rows of every ldmatrix 8x8 tile hit distinct bank
+// groups). Fragments come from ldmatrix.x4 (Q as A, K as B) and
+// ldmatrix.x4.trans (V as B of P.V), so no transposing stores are needed.
 template <int DH>
-__global__ void __launch_bounds__(256) attn_bf16_kernel(const __nv_bfloat16 *__restrict__ qkv,
-                                                         __nv_bfloat16 *__restrict__ out, int S,
-                                                         int H, float scale_log2) {
+__global__ void __launch_bounds__(256, DH == 64 ? 2 : 1) attn_bf16_kernel(const __nv_bfloat16 *__restrict__ qkv,
+                                                            __nv_bfloat16 *__restrict__ out,
+                                                            int S, int H, float scale_log2) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int KS = DH + 8;  // padded K row (bf16 elements)
-  const int VS = S + 8;   // padded V^T row
-  __nv_bfloat16 *Ks = reinterpret_cast<__nv_bfloat16 *>(smem);
-  __nv_bfloat16 *Vt = Ks + S * KS;
+  constexpr int LD = DH + 8;
+  __nv_bfloat16 *Qs = reinterpret_cast<__nv_bfloat16 *>(smem);
+  __nv_bfloat16 *Ks = Qs + S * LD;
+  __nv_bfloat16 *Vs = Ks + S * LD;
   const int seq = blockIdx.x / H, h = blockIdx.x % H;
   const int D = H * DH;
   const size_t row0 = (size_t)seq * S;
-  const __nv_bfloat16 *base = qkv + row0 * 3 * D;
-  // stage K (row-major) and V (transposed), 16 bytes per load
+  const __nv_bfloat16 *base = qkv + row0 * 3 * D + h * DH;
   constexpr int kVec = DH / 8;
   for (int i = threadIdx.x; i < S * kVec; i += blockDim.x) {
     const int j = i / kVec, c = (i % kVec) * 8;
-    const __nv_bfloat16 *rp = base + (size_t)j * 3 * D + h * DH + c;
-    uint4 kv = __ldg(reinterpret_cast<const uint4 *>(rp + D));
-    *reinterpret_cast<uint4 *>(Ks + j * KS + c) = kv;
-    uint4 vv = __ldg(reinterpret_cast<const uint4 *>(rp + 2 * D));
-    const __nv_bfloat16 *ve = reinterpret_cast<const __nv_bfloat16 *>(&vv);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) Vt[(c + e) * VS + j] = ve[e];
+    const __nv_bfloat16 *rp = base + (size_t)j * 3 * D + c;
+    cp_async16(Qs + j * LD + c, rp);
+    cp_async16(Ks + j * LD + c, rp + D);
+    cp_async16(Vs + j * LD + c, rp + 2 * D);
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int nwarps = blockDim.x >> 5;
+  const int lr = lane & 7, lm = lane >> 3;  // ldmatrix: row within tile, tile index
   for (int rb = warp; rb < S / 16; rb += nwarps) {
     const int r0 = rb * 16;
-    // Q fragments straight from global (read once)
     uint32_t qa[DH / 16][4];
-    const __nv_bfloat16 *q0 = base + (size_t)(r0 + g) * 3 * D + h * DH;
-    const __nv_bfloat16 *q1 = q0 + (size_t)8 * 3 * D;
 #pragma unroll
-    for (int ks = 0; ks < DH / 16; ++ks) {
-      qa[ks][0] = __ldg(reinterpret_cast<const uint32_t *>(q0 + ks * 16 + 2 * t));
-      qa[ks][1] = __ldg(reinterpret_cast<const uint32_t *>(q1 + ks * 16 + 2 * t));
-      qa[ks][2] = __ldg(reinterpret_cast<const uint32_t *>(q0 + ks * 16 + 8 + 2 * t));
-      qa[ks][3] = __ldg(reinterpret_cast<const uint32_t *>(q1 + ks * 16 + 8 + 2 * t));
-    }
+    for (int ks = 0; ks < DH / 16; ++ks)
+      ldsm_x4(qa[ks], Qs + (r0 + (lane & 15)) * LD + ks * 16 + (lane >> 4) * 8);
     float o[DH / 8][4];
 #pragma unroll
     for (int i = 0; i < DH / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
@@ -84,14 +96,15 @@ __global__ void __launch_bounds__(256) attn_bf16_kernel(const __nv_bfloat16 *__r
     for (int kv0 = 0; kv0 < S; kv0 += 64) {
       float s[8][4];
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-        const __nv_bfloat16 *kr = Ks + (kv0 + nt * 8 + g) * KS;
+      for (int nt = 0; nt < 8; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {      // pairs of 8-key n-tiles
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks) {
-          uint32_t b0 = *reinterpret_cast<const uint32_t *>(kr + ks * 16 + 2 * t);
-          uint32_t b1 = *reinterpret_cast<const uint32_t *>(kr + ks * 16 + 8 + 2 * t);
-          mma_bf16_16816(s[nt], qa[ks], b0, b1);
+          uint32_t b[4];  // tiles: (keys +0..7, dims +0..7), (+0..7, +8..15), (+8..15, +0..7), (+8..15, +8..15)
+          ldsm_x4(b, Ks + (kv0 + np * 16 + (lm >> 1) * 8 + lr) * LD + ks * 16 + (lm & 1) * 8);
+          mma_bf16_16816(s[2 * np], qa[ks], b[0], b[1]);
+          mma_bf16_16816(s[2 * np + 1], qa[ks], b[2], b[3]);
         }
       }
       float mx0 = m0, mx1 = m1;
@@ -120,8 +133,10 @@ __global__ void __launch_bounds__(256) attn_bf16_kernel(const __nv_bfloat16 *__r
       uint32_t pa[4][4];
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
-        float p0 = exp2f(s[nt][0] * scale_log2 - sm0), p1 = exp2f(s[nt][1] * scale_log2 - sm0);
-        float p2 = exp2f(s[nt][2] * scale_log2 - sm1), p3 = exp2f(s[nt][3] * scale_log2 - sm1);
+        float p0 = exp2f(fmaf(s[nt][0], scale_log2, -sm0));
+        float p1 = exp2f(fmaf(s[nt][1], scale_log2, -sm0));
+        float p2 = exp2f(fmaf(s[nt][2], scale_log2, -sm1));
+        float p3 = exp2f(fmaf(s[nt][3], scale_log2, -sm1));
         l0 += p0 + p1;
         l1 += p2 + p3;
         const int j = nt >> 1, hi = nt & 1;
@@ -129,13 +144,13 @@ __global__ void __launch_bounds__(256) attn_bf16_kernel(const __nv_bfloat16 *__r
         pa[j][hi ? 3 : 1] = pack2(p2, p3);
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 4; ++j) {          // 16-key k-steps
 #pragma unroll
-        for (int nt = 0; nt < DH / 8; ++nt) {
-          const __nv_bfloat16 *vr = Vt + (nt * 8 + g) * VS + kv0 + j * 16;
-          uint32_t b0 = *reinterpret_cast<const uint32_t *>(vr + 2 * t);
-          uint32_t b1 = *reinterpret_cast<const uint32_t *>(vr + 8 + 2 * t);
-          mma_bf16_16816(o[nt], pa[j], b0, b1);
+        for (int dp = 0; dp < DH / 16; ++dp) {  // pairs of 8-dim n-tiles
+          uint32_t b[4];  // tiles (keys +0..7, dims +0..7), (+8..15, +0..7), (+0..7, +8..15), (+8..15, +8..15)
+          ldsm_x4_t(b, Vs + (kv0 + j * 16 + (lm & 1) * 8 + lr) * LD + dp * 16 + (lm >> 1) * 8);
+          mma_bf16_16816(o[2 * dp], pa[j], b[0], b[1]);
+          mma_bf16_16816(o[2 * dp + 1], pa[j], b[2], b[3]);
         }
       }
     }
@@ -153,6 +168,7 @@ __global__ void __launch_bounds__(256) attn_bf16_kernel(const __nv_bfloat16 *__r
     }
   }
 }
+
 
 // fp32 reference-order attention: one warp per (sequence, head, query row).
 __global__ void attn_f32_kernel(const float *__restrict__ qkv, float *__restrict__ out, int n_seqs,
@@ -205,7 +221,7 @@ cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
                            int dh, cudaStream_t s) {
   if (n_seqs <= 0) return cudaSuccess;
   if (S % 64 != 0 || dh % 16 != 0) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)S * (dh + 8) * 2 + (size_t)dh * (S + 8) * 2;
+  const size_t smem = (size_t)3 * S * (dh + 8) * 2;
   const int threads = std::min(256, std::max(32, (S / 16) * 32));
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)dh);
   cudaError_t e;

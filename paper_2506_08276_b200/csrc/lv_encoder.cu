@@ -631,6 +631,16 @@ int lv_gemm_bf16(const void *A, const void *W, const float *bias, const void *re
                  (cudaStream_t)stream);
 }
 
+int lv_attention_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int32_t H,
+                      int32_t dh, void *stream) {
+  LV_REQUIRE(qkv && out, LV_ERR_USAGE, "lv_attention_bf16: null argument");
+  LV_REQUIRE(S % 64 == 0 && (dh == 64 || dh == 128), LV_ERR_USAGE,
+             "lv_attention_bf16: need S % 64 == 0 and dh in {64, 128}");
+  LV_CHECK_CUDA(attention_bf16((const __nv_bfloat16 *)qkv, (__nv_bfloat16 *)out, n_seqs, S, H, dh,
+                               (cudaStream_t)stream));
+  return LV_OK;
+}
+
 int lv_set_gemm_mode(int mode) {
   const int prev = g_gemm_mode;
   g_gemm_mode = mode;

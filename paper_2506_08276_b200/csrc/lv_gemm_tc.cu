@@ -432,6 +432,64 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], const fl
   }
 }
 
+// Per-chunk epilogue operands: 32 bias values and (residual epilogue) 32 bf16
+// residual values of the thread's row.
+struct EpiOperands {
+  float4 b[8];
+  uint4 res[4];
+};
+
+__device__ __forceinline__ void load_operands(EpiOperands &o, const float *bias,
+                                              const __nv_bfloat16 *residual, int row, int gn,
+                                              int N, int epi, bool live) {
+  const float4 *b4 = reinterpret_cast<const float4 *>(bias + gn);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o.b[j] = __ldg(b4 + j);
+  if (epi == EPI_BIAS_RESIDUAL && live) {
+    const uint4 *rp = reinterpret_cast<const uint4 *>(residual + (size_t)row * N + gn);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o.res[j] = __ldg(rp + j);
+  }
+}
+
+__device__ __forceinline__ void epilogue_apply(const uint32_t (&r)[32], const EpiOperands &o,
+                                               __nv_bfloat16 *out, int row, int gn, int N,
+                                               int epi) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    v[4 * j + 0] = __uint_as_float(r[4 * j + 0]) + o.b[j].x;
+    v[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + o.b[j].y;
+    v[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + o.b[j].z;
+    v[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + o.b[j].w;
+  }
+  if (epi == EPI_BIAS_GELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+  } else if (epi == EPI_BIAS_RESIDUAL) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&o.res[j]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = __bfloat1622float2(h[e]);
+        v[8 * j + 2 * e] += f.x;
+        v[8 * j + 2 * e + 1] += f.y;
+      }
+    }
+  }
+  uint4 *op = reinterpret_cast<uint4 *>(out + (size_t)row * N + gn);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 u;
+    u.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+    u.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+    u.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+    u.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+    op[j] = u;
+  }
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
@@ -550,16 +608,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int tile = pair; tile < num_tiles; tile += n_pairs) {
       const int m0 = (tile / n_tiles) * 256 + (int)rank * 128;
       const int n0 = (tile % n_tiles) * BN;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       const int row = m0 + q * 32 + lane;
       const bool live = row < M;
+      // operands of chunk 0 are fetched before waiting for the accumulator, and
+      // those of chunk c+1 while chunk c is processed: their latency hides
+      // behind the MMA / TMEM loads instead of stalling the epilogue.
+      EpiOperands nxt;
+      load_operands(nxt, bias, residual, row, n0 + half * kCols, N, epi, live);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < kCols; c += 32) {
         const int col = half * kCols + c;
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col), r);
-        if (live) epilogue_chunk(r, bias, residual, out, row, n0 + col, N, epi);
+        const EpiOperands cur = nxt;
+        if (c + 32 < kCols) load_operands(nxt, bias, residual, row, n0 + col + 32, N, epi, live);
+        if (live) epilogue_apply(r, cur, out, row, n0 + col, N, epi);
       }
       tc_fence_before();
       __syncwarp();

@@ -27,7 +27,8 @@ from .encoder import EncoderProvider, GpuEncoder, TokenStore
 from .errors import InvalidArgumentError
 from .graph import load_graph, save_graph
 from .pq import load_pq, save_pq
-from .search import MatrixSource, ProviderSource, SearchParams, device_index_for
+from .search import (MatrixSource, ProviderSource, SearchParams, build_embedding_cache,
+                     device_index_for)
 
 
 def build(tokens, encoder: GpuEncoder, out_dir=None, params: GpuBuildParams | None = None,
@@ -65,7 +66,8 @@ class LeannSearcher:
     """A resident index (graph + PQ + token store + encoder) on one GPU."""
 
     def __init__(self, graph, pq_model, pq_codes, encoder: GpuEncoder, tokens,
-                 matrix=None, rerank_percent: float = 30.0, batch_size: int = 64) -> None:
+                 matrix=None, rerank_percent: float = 30.0, batch_size: int = 64,
+                 cache_percent: float | None = None) -> None:
         self.graph = graph
         self.pq_model = pq_model
         self.pq_codes = pq_codes
@@ -77,6 +79,10 @@ class LeannSearcher:
         self.batch_size = batch_size
         self.device_index = device_index_for(graph, pq_model, pq_codes)
         self._out = None
+        # hub-node embedding cache (build_embedding_cache, search.py:130-142):
+        # pinned exact vectors, results-transparent, computed once at open time
+        self.cache = (build_embedding_cache(graph, cache_percent)
+                      if cache_percent else None)
 
     @classmethod
     def open(cls, index_dir, encoder: GpuEncoder, token_bytes: int = 2, **kw) -> "LeannSearcher":
@@ -119,7 +125,7 @@ class LeannSearcher:
             if self.matrix is None:
                 raise InvalidArgumentError("recompute=False needs a resident embedding matrix")
             source = MatrixSource(self.matrix)
-        out = self.device_index.search_device(Q, params, source, qn=None,
+        out = self.device_index.search_device(Q, params, source, qn=None, cache=self.cache,
                                               max_inflight=max_inflight, out=self._out)
         self._out = out
         B = Q.shape[0]

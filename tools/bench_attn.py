@@ -1,0 +1,35 @@
+"""Microbenchmark of the encoder attention (config-2 shape by default), CUDA events."""
+import sys
+import torch
+sys.path.insert(0, "/root/repo")
+import __graft_entry__ as ge  # noqa: E402
+ge.build()
+from paper_2506_08276_b200 import _lib  # noqa: E402
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1300
+S, H, dh = 256, 12, 64
+qkv = torch.randn(n * S, 3 * H * dh, device="cuda").to(torch.bfloat16)
+out = torch.empty(n * S, H * dh, device="cuda", dtype=torch.bfloat16)
+st = torch.cuda.current_stream()
+for _ in range(3):
+    _lib.check(_lib.lib().lv_attention_bf16(qkv.data_ptr(), out.data_ptr(), n, S, H, dh, st.cuda_stream))
+ts = []
+for _ in range(5):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    _lib.check(_lib.lib().lv_attention_bf16(qkv.data_ptr(), out.data_ptr(), n, S, H, dh, st.cuda_stream))
+    e1.record(st)
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+t = sorted(ts)[2]
+fl = 4.0 * S * S * dh * H * n
+print(f"attention n={n} S={S} H={H} dh={dh}: {t*1e3:.1f} us  {fl / t / 1e9:.1f} TF/s  "
+      f"{3 * n * S * H * dh * 2 * 1.0 / t / 1e6:.0f} GB/s of qkv")
+q = qkv.view(n, S, 3, H, dh)
+for _ in range(2):
+    torch.nn.functional.scaled_dot_product_attention(q[:, :, 0].transpose(1, 2), q[:, :, 1].transpose(1, 2), q[:, :, 2].transpose(1, 2))
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(st)
+torch.nn.functional.scaled_dot_product_attention(q[:, :, 0].transpose(1, 2), q[:, :, 1].transpose(1, 2), q[:, :, 2].transpose(1, 2))
+e1.record(st)
+torch.cuda.synchronize()
+print(f"torch sdpa (incl. strided views): {e0.elapsed_time(e1)*1e3:.1f} us")
