@@ -196,6 +196,10 @@ int lv_attention_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int
 /* GEMM kernel selection: 0 = auto (2-CTA cta_group::2 kernel when N % 256 == 0),
  * 1 = 1-CTA kernel only. Returns the previous mode. */
 int lv_set_gemm_mode(int mode);
+/* Attention kernel selection: 0 = auto (tcgen05/TMEM kernel for dh == 64 and
+ * S in {128, 256}, else the mma.sync kernel), 1 = mma.sync kernel only.
+ * Returns the previous mode. */
+int lv_set_attention_mode(int mode);
 
 #ifdef __cplusplus
 }

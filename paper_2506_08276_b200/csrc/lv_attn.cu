@@ -13,6 +13,7 @@
 #include <cfloat>
 
 #include "lv_kernels.cuh"
+#include "lv_tc.cuh"
 
 namespace lv {
 namespace {
@@ -170,6 +171,254 @@ __global__ void __launch_bounds__(256, DH == 64 ? 2 : 1) attn_bf16_kernel(const 
 }
 
 
+// ---------------------------------------------------------------------------
+// attn_tc_kernel: the same attention on the 5th-gen tensor cores.
+//
+// Work item = one (sequence, head); S in {128, 256}, dh = 64. Persistent, one
+// CTA per SM, warp-specialised:
+//   warp 0      TMA: Q, K, V of an item ([S][64] bf16 boxes of the qkv rows,
+//               128-byte swizzle) into a 2-stage shared-memory ring;
+//   warp 1      one lane issues tcgen05.mma: per 128-row Q tile t,
+//                 S_t = Q_t . K^T   (SS, M=128, N=S, K=64)   -> TMEM region r
+//                 O_t = P_t . V     (TS, M=128, N=64, K=S)   -> same region
+//               with P_t read from TMEM (A operand) and V as an MN-major
+//               shared-memory operand (no transpose anywhere);
+//   warps 2-9   two softmax groups of 4 warps (group r owns TMEM region r =
+//               256 columns; tiles alternate between the groups so the MMA of
+//               one tile overlaps the softmax of the other). A thread owns one
+//               query row: pass 1 row max over S columns, pass 2
+//               p = 2^(s*c - max*c) (MUFU ex2), row sum in fp32, P packed to
+//               bf16 and written back over the consumed score columns
+//               (tcgen05.st); after the P.V MMA it reads O, scales by 1/sum and
+//               stores its 128-byte head slice of the context row.
+// No mask (every passage is exactly S tokens) and no online rescaling (a row
+// of scores fits in TMEM). Batch-invariant: each item is a fixed-order
+// computation independent of the launch.
+namespace atc {
+constexpr int kThreads = 64 + 8 * 32;
+template <int S>
+struct Cfg {
+  static constexpr int kTileBytes = S * 128;  // [S][64] bf16
+  static constexpr int kStageBytes = 3 * kTileBytes;
+  static constexpr int kStages = 2;
+  static constexpr int kQTiles = S / 128;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+};
+}  // namespace atc
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int S>
+__global__ void __launch_bounds__(atc::kThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out,
+                   int n_items, int H, float scale_log2) {
+  using namespace tc;
+  using C = atc::Cfg<S>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStageBytes);
+  uint64_t *empty = full + 2;
+  uint64_t *s_full = empty + 2;
+  uint64_t *p_full = s_full + 2;
+  uint64_t *o_full = p_full + 2;
+  uint64_t *r_free = o_full + 2;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(r_free + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&r_free[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const int D = H * 64;
+  const int n_local = n_items > (int)blockIdx.x
+                          ? (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
+                          : 0;
+  const int total = n_local * C::kQTiles;  // Q tiles this CTA processes
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tm) : "memory");
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      for (int i = 0; i < n_local; ++i) {
+        const int st = i & 1;
+        mbar_wait(&empty[st], ((i >> 1) & 1) ^ 1);
+        const int item = (int)blockIdx.x + i * (int)gridDim.x;
+        const int seq = item / H, h = item - seq * H;
+        uint8_t *base = smem + st * C::kStageBytes;
+        mbar_expect_tx(&full[st], C::kStageBytes);
+        tma_load_2d(base, &tm, &full[st], h * 64, seq * S, pol);
+        tma_load_2d(base + C::kTileBytes, &tm, &full[st], D + h * 64, seq * S, pol);
+        tma_load_2d(base + 2 * C::kTileBytes, &tm, &full[st], 2 * D + h * 64, seq * S, pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16(128, S);
+      constexpr uint32_t idesc_o = idesc_bf16(128, 64, true);
+      auto issue_s = [&](int j) {
+        const int i = j / C::kQTiles, t = j % C::kQTiles, r = j & 1;
+        if (t == 0) mbar_wait(&full[i & 1], (i >> 1) & 1);
+        mbar_wait(&r_free[r], ((j >> 1) & 1) ^ 1);
+        fence_after();
+        const uint8_t *base = smem + (i & 1) * C::kStageBytes;
+        const uint64_t a = sw128_desc(smem_u32(base + t * 128 * 128));
+        const uint64_t b = sw128_desc(smem_u32(base + C::kTileBytes));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) umma_ss(tmem + r * 256, a + 2 * k, b + 2 * k, idesc_s, k);
+        umma_commit(&s_full[r]);
+      };
+      auto issue_pv = [&](int j) {
+        const int i = j / C::kQTiles, t = j % C::kQTiles, r = j & 1;
+        mbar_wait(&p_full[r], (j >> 1) & 1);
+        fence_after();
+        const uint8_t *base = smem + (i & 1) * C::kStageBytes;
+        const uint64_t v = sw128_desc(smem_u32(base + 2 * C::kTileBytes), 1024, 16);
+#pragma unroll
+        for (int k = 0; k < S / 16; ++k)  // 16 keys = 2 swizzle atoms (2048 B) of V per step
+          umma_ts(tmem + r * 256 + S / 2, tmem + r * 256 + 8 * k, v + (uint64_t)(128 * k), idesc_o,
+                  k);
+        umma_commit(&o_full[r]);
+        if (t == C::kQTiles - 1) umma_commit(&empty[i & 1]);
+      };
+      if (total > 0) issue_s(0);
+      if (total > 1) issue_s(1);
+      for (int j = 0; j < total; ++j) {
+        issue_pv(j);
+        if (j + 2 < total) issue_s(j + 2);
+      }
+    }
+  } else {
+    const int g = (warp - 2) >> 2;  // softmax group = TMEM region
+    const int q = warp & 3;         // TMEM lane quarter
+    const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * 256);
+    for (int j = g; j < total; j += 2) {
+      const uint32_t ph = (uint32_t)(j >> 1) & 1;
+      mbar_wait(&s_full[g], ph);
+      fence_after();
+      // pass 1: row max
+      float mx = -FLT_MAX;
+#pragma unroll 1
+      for (int c = 0; c < S / 32; c += 2) {
+        uint32_t r0[32], r1[32];
+        tmem_ld32_nowait(tb + 32 * c, r0);
+        tmem_ld32_nowait(tb + 32 * c + 32, r1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          mx = fmaxf(mx, fmaxf(__uint_as_float(r0[e]), __uint_as_float(r1[e])));
+      }
+      const float mc = mx * scale_log2;
+      // pass 2: p = 2^(s*c - max*c), row sum, P (bf16) over the consumed columns
+      float sum = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < S / 32; ++c) {
+        uint32_t r0[32];
+        tmem_ld32(tb + 32 * c, r0);
+        uint32_t w[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float p0 = ex2_approx(fmaf(__uint_as_float(r0[2 * e]), scale_log2, -mc));
+          const float p1 = ex2_approx(fmaf(__uint_as_float(r0[2 * e + 1]), scale_log2, -mc));
+          sum += p0 + p1;
+          w[e] = pack_bf16(p0, p1);
+        }
+        tmem_st16(tb + 16 * c, w);
+      }
+      tmem_st_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[g]);
+      // epilogue: O / sum -> context row slice
+      const int i = j / C::kQTiles, t = j % C::kQTiles;
+      const int item = (int)blockIdx.x + i * (int)gridDim.x;
+      const int seq = item / H, h = item - seq * H;
+      const size_t row = (size_t)seq * S + t * 128 + q * 32 + lane;
+      mbar_wait(&o_full[g], ph);
+      fence_after();
+      uint32_t o0[32], o1[32];
+      tmem_ld32_nowait(tb + S / 2, o0);
+      tmem_ld32_nowait(tb + S / 2 + 32, o1);
+      tmem_ld_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r_free[g]);
+      const float inv = 1.f / sum;
+      uint4 *op = reinterpret_cast<uint4 *>(out + row * D + h * 64);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 u;
+        u.x = pack_bf16(__uint_as_float(o0[8 * v + 0]) * inv, __uint_as_float(o0[8 * v + 1]) * inv);
+        u.y = pack_bf16(__uint_as_float(o0[8 * v + 2]) * inv, __uint_as_float(o0[8 * v + 3]) * inv);
+        u.z = pack_bf16(__uint_as_float(o0[8 * v + 4]) * inv, __uint_as_float(o0[8 * v + 5]) * inv);
+        u.w = pack_bf16(__uint_as_float(o0[8 * v + 6]) * inv, __uint_as_float(o0[8 * v + 7]) * inv);
+        op[v] = u;
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 u;
+        u.x = pack_bf16(__uint_as_float(o1[8 * v + 0]) * inv, __uint_as_float(o1[8 * v + 1]) * inv);
+        u.y = pack_bf16(__uint_as_float(o1[8 * v + 2]) * inv, __uint_as_float(o1[8 * v + 3]) * inv);
+        u.z = pack_bf16(__uint_as_float(o1[8 * v + 4]) * inv, __uint_as_float(o1[8 * v + 5]) * inv);
+        u.w = pack_bf16(__uint_as_float(o1[8 * v + 6]) * inv, __uint_as_float(o1[8 * v + 7]) * inv);
+        op[4 + v] = u;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+template <int S>
+cudaError_t launch_attn_tc(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int H,
+                           cudaStream_t s) {
+  using C = atc::Cfg<S>;
+  CUtensorMap tm;
+  const uint64_t D3 = (uint64_t)3 * H * 64;
+  if (!make_tma_2d_bf16(&tm, qkv, D3, (uint64_t)n_seqs * S, D3 * 2, 64, S))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<S>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int items = n_seqs * H;
+  const int grid = std::min(items, tc_gemm_num_sms());
+  attn_tc_kernel<S><<<grid, atc::kThreads, C::kSmem, s>>>(tm, out, items, H,
+                                                          1.4426950408889634f / 8.0f);
+  note_launch();
+  return cudaGetLastError();
+}
+
+
 // fp32 reference-order attention: one warp per (sequence, head, query row).
 __global__ void attn_f32_kernel(const float *__restrict__ qkv, float *__restrict__ out, int n_seqs,
                                 int S, int H, int dh, float scale) {
@@ -217,10 +466,17 @@ __global__ void attn_f32_kernel(const float *__restrict__ qkv, float *__restrict
 
 }  // namespace
 
+int g_attn_mode = 0;
+
 cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S, int H,
                            int dh, cudaStream_t s) {
   if (n_seqs <= 0) return cudaSuccess;
   if (S % 64 != 0 || dh % 16 != 0) return cudaErrorInvalidValue;
+  if (g_attn_mode == 0 && dh == 64 && (S == 128 || S == 256)) {
+    if (((uintptr_t)qkv & 15) != 0 || ((uintptr_t)out & 15) != 0) return cudaErrorInvalidValue;
+    return S == 256 ? launch_attn_tc<256>(qkv, out, n_seqs, H, s)
+                    : launch_attn_tc<128>(qkv, out, n_seqs, H, s);
+  }
   const size_t smem = (size_t)3 * S * (dh + 8) * 2;
   const int threads = std::min(256, std::max(32, (S / 16) * 32));
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)dh);

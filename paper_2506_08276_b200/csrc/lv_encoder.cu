@@ -647,6 +647,12 @@ int lv_set_gemm_mode(int mode) {
   return prev;
 }
 
+int lv_set_attention_mode(int mode) {
+  const int prev = g_attn_mode;
+  g_attn_mode = mode;
+  return prev;
+}
+
 int lv_encoder_profile(lv_encoder *enc, int enable) {
   LV_REQUIRE(enc, LV_ERR_USAGE, "null encoder");
   enc->profile = enable != 0;

@@ -3,6 +3,7 @@
 // T = n_seqs * seq_len; every kernel is batch-invariant (a row's result never
 // depends on which other rows share the launch): fixed K order, no split-K.
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include "lv_common.cuh"
@@ -24,6 +25,10 @@ int tc_gemm(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
             const __nv_bfloat16 *residual, __nv_bfloat16 *out, int M, int N, int K, int epi,
             cudaStream_t s);
 int tc_gemm_num_sms();
+// Row-major bf16 [rows][cols] tensor map (row stride in bytes), box
+// (box_cols x box_rows), 128-byte swizzle (box_cols * 2 must be 128).
+bool make_tma_2d_bf16(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows,
+                      uint64_t row_stride_bytes, int box_cols, int box_rows);
 extern int g_gemm_mode;  // 0 auto (2-CTA pair kernel when N % 256 == 0), 1 force 1-CTA
 
 // ---- fp32 SIMT GEMM (parity mode, lv_encoder.cu): same contract in fp32.
@@ -34,6 +39,7 @@ cudaError_t f32_gemm(const float *A, const float *W, const float *bias, const fl
 // each), out [T][H*dh]; bidirectional softmax(q k^T / sqrt(dh)) v per sequence.
 cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S,
                            int H, int dh, cudaStream_t s);
+extern int g_attn_mode;  // 0 auto (tcgen05 kernel for dh 64, S 128/256), 1 mma.sync kernel
 cudaError_t attention_f32(const float *qkv, float *out, int n_seqs, int S, int H, int dh,
                           cudaStream_t s);
 

@@ -124,17 +124,24 @@ def test_encoder_device_tokens_and_provider(lv):
     assert np.array_equal(prov.embed_batch(reqs), host[[3, 7]])
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("n,S,H,dh", [(3, 64, 4, 64), (5, 256, 12, 64), (2, 128, 8, 128),
-                                      (2, 512, 16, 64)])
-def test_attention_bf16_matches_torch(lv, n, S, H, dh):
+                                      (2, 512, 16, 64), (7, 128, 4, 64), (61, 256, 12, 64),
+                                      (300, 128, 4, 64)])
+def test_attention_bf16_matches_torch(lv, n, S, H, dh, mode):
+    """mode 0: tcgen05/TMEM kernel where it applies (dh 64, S 128/256); mode 1: mma.sync."""
     torch = _torch()
     from paper_2506_08276_b200 import _lib
     g = torch.Generator(device="cuda").manual_seed(n * 31 + S)
     qkv = (torch.randn(n * S, 3 * H * dh, device="cuda", generator=g)).to(torch.bfloat16)
     out = torch.empty(n * S, H * dh, device="cuda", dtype=torch.bfloat16)
-    _lib.check(_lib.lib().lv_attention_bf16(qkv.data_ptr(), out.data_ptr(), n, S, H, dh,
-                                            torch.cuda.current_stream().cuda_stream))
-    torch.cuda.synchronize()
+    prev = _lib.lib().lv_set_attention_mode(mode)
+    try:
+        _lib.check(_lib.lib().lv_attention_bf16(qkv.data_ptr(), out.data_ptr(), n, S, H, dh,
+                                                torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+    finally:
+        _lib.lib().lv_set_attention_mode(prev)
     q, k, v = qkv.float().view(n, S, 3, H, dh).unbind(2)
     ref = torch.nn.functional.scaled_dot_product_attention(
         q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2)).transpose(1, 2).reshape(n * S, -1)
