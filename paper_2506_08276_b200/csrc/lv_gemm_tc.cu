@@ -247,10 +247,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 // arrive on the leader's barrier. Per SM this loads (128 + 128) x 64 x 2 bytes
 // per 128 x 256 x 64 MACs: 1.5x the MACs per L2 byte of the 1-CTA kernel,
 // whose 50%-busy tensor pipe was bound by TMA/L2 throughput.
-constexpr int kStages2 = 6;
+constexpr int kStages2 = 5;
 constexpr int kHalfBytes = 128 * kBK * 2;          // 16 KB: A or B half per stage
 constexpr int kStageBytes2 = 2 * kHalfBytes;        // per CTA
-constexpr int kSmem2 = kStages2 * kStageBytes2 + 1024 + 256;
+// epilogue staging: per epilogue warp two [32 rows][64 cols] bf16 boxes (4 KB
+// each, 128-byte swizzle) — residual tile in (TMA load), output tile out (TMA store)
+constexpr int kBoxBytes = 32 * 64 * 2;
+constexpr int kStagingBytes = kEpiWarps * 2 * kBoxBytes;
+constexpr int kSmem2 = kStages2 * kStageBytes2 + kStagingBytes + 1024 + 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -399,21 +403,23 @@ __device__ __forceinline__ void epilogue_apply(const uint32_t (&r)[32], const Ep
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-                        const float *__restrict__ bias,
-                        const __nv_bfloat16 *__restrict__ residual,
-                        __nv_bfloat16 *__restrict__ out, int epi) {
+                        const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmO,
+                        const __grid_constant__ CUtensorMap tmR, int M, int N, int K,
+                        const float *__restrict__ bias, int epi) {
   constexpr int BN = 256;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
   uint8_t *sB = smem + kStages2 * kHalfBytes;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + kStages2 * kHalfBytes);
+  uint8_t *sStage = sB + kStages2 * kHalfBytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sStage + kStagingBytes);
   uint64_t *empty = full + kStages2;
   uint64_t *tfull = empty + kStages2;
   uint64_t *tempty = tfull + 2;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint64_t *rbar = tempty + 2;  // [kEpiWarps][2] residual-box arrivals
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(rbar + 2 * kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -428,6 +434,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * kEpiWarps);
     }
+    for (int a = 0; a < 2 * kEpiWarps; ++a) mbar_init(&rbar[a], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -504,41 +511,124 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else {
+    // Epilogue: each warp owns 32 accumulator rows (its TMEM lane quarter) x
+    // 128 columns (its half), processed as two 64-column boxes. A box goes
+    // TMEM -> registers (+bias, GELU / +residual) -> swizzled shared-memory
+    // staging -> one TMA store; the residual box arrives by TMA one box ahead.
+    // Every global access is a coalesced bulk transfer (a thread-per-row
+    // st.global would touch 32 cache lines per instruction).
     const int ew = warp - 2;
     const int q = warp & 3;
     const int half = ew >> 2;
-    constexpr int kCols = BN / 2;
+    const bool has_res = epi == EPI_BIAS_RESIDUAL;
+    uint8_t *stg = sStage + ew * 2 * kBoxBytes;
+    uint64_t *rb = rbar + 2 * ew;
+    uint32_t rph = 0;  // parity bit per buffer
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
     const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
+    uint64_t pol_r = 0;
+    if (has_res) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_r));
+    auto box_coords = [&](int tile, int b, int &x, int &y) {
+      y = (tile / n_tiles) * 256 + (int)rank * 128 + q * 32;
+      x = (tile % n_tiles) * BN + half * 128 + b * 64;
+    };
+    if (has_res && lane == 0 && pair < num_tiles) {
+      int x, y;
+      box_coords(pair, 0, x, y);
+      mbar_expect_tx(&rb[0], kBoxBytes);
+      tma_load_2d(stg, &tmR, &rb[0], x, y, pol_r);
+    }
+    // 16-byte chunk c of row r of a 128-byte-swizzled box
+    const uint32_t row_off = (uint32_t)lane * 128;
+    const uint32_t sw = (uint32_t)(lane & 7);
     int acc = 0;
     uint32_t acc_phase = 0;
+    int blk = 0;
     for (int tile = pair; tile < num_tiles; tile += n_pairs) {
-      const int m0 = (tile / n_tiles) * 256 + (int)rank * 128;
-      const int n0 = (tile % n_tiles) * BN;
-      const int row = m0 + q * 32 + lane;
-      const bool live = row < M;
-      // operands of chunk 0 are fetched before waiting for the accumulator, and
-      // those of chunk c+1 while chunk c is processed: their latency hides
-      // behind the MMA / TMEM loads instead of stalling the epilogue.
-      EpiOperands nxt;
-      load_operands(nxt, bias, residual, row, n0 + half * kCols, N, epi, live);
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
 #pragma unroll 1
-      for (int c = 0; c < kCols; c += 32) {
-        const int col = half * kCols + c;
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col), r);
-        const EpiOperands cur = nxt;
-        if (c + 32 < kCols) load_operands(nxt, bias, residual, row, n0 + col + 32, N, epi, live);
-        if (live) epilogue_apply(r, cur, out, row, n0 + col, N, epi);
+      for (int b = 0; b < 2; ++b, ++blk) {
+        const int buf = blk & 1;
+        uint8_t *box = stg + buf * kBoxBytes;
+        int x, y;
+        box_coords(tile, b, x, y);
+        uint32_t r[64];
+        {
+          uint32_t(&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
+          uint32_t(&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32]);
+          const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) +
+                              (uint32_t)(acc * BN + half * 128 + b * 64);
+          tmem_ld32_nowait(ta, r0);
+          tmem_ld32_nowait(ta + 32, r1);
+          tmem_ld_wait();
+        }
+        if (b == 1) {  // accumulator fully read: the MMA of the next tile may reuse it
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
+        }
+        // next box's residual into the other buffer (its previous TMA store
+        // must have finished reading it)
+        if (lane == 0) {
+          if (has_res) {
+            const int nt = b == 0 ? tile : tile + n_pairs;
+            if (nt < num_tiles) {
+              bulk_wait_read<0>();
+              int nx, ny;
+              box_coords(nt, b ^ 1, nx, ny);
+              mbar_expect_tx(&rb[buf ^ 1], kBoxBytes);
+              tma_load_2d(stg + (buf ^ 1) * kBoxBytes, &tmR, &rb[buf ^ 1], nx, ny, pol_r);
+            }
+          } else {
+            bulk_wait_read<1>();  // the store issued from this buffer two boxes ago
+          }
+        }
+        __syncwarp();
+        if (has_res) {
+          mbar_wait(&rb[buf], (rph >> buf) & 1);
+          rph ^= 1u << buf;
+        }
+        const float4 *b4 = reinterpret_cast<const float4 *>(bias + x);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // 8 columns per 16-byte chunk
+          const float4 bl = __ldg(b4 + 2 * c), bh = __ldg(b4 + 2 * c + 1);
+          float v[8] = {__uint_as_float(r[8 * c + 0]) + bl.x, __uint_as_float(r[8 * c + 1]) + bl.y,
+                        __uint_as_float(r[8 * c + 2]) + bl.z, __uint_as_float(r[8 * c + 3]) + bl.w,
+                        __uint_as_float(r[8 * c + 4]) + bh.x, __uint_as_float(r[8 * c + 5]) + bh.y,
+                        __uint_as_float(r[8 * c + 6]) + bh.z, __uint_as_float(r[8 * c + 7]) + bh.w};
+          uint4 *cp = reinterpret_cast<uint4 *>(box + row_off + (((uint32_t)c ^ sw) << 4));
+          if (epi == EPI_BIAS_GELU) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = gelu_erf(v[e]);
+          } else if (has_res) {
+            const uint4 u = *cp;
+            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h[e]);
+              v[2 * e] += f.x;
+              v[2 * e + 1] += f.y;
+            }
+          }
+          uint4 o;
+          o.x = pack_bf16(v[0], v[1]);
+          o.y = pack_bf16(v[2], v[3]);
+          o.z = pack_bf16(v[4], v[5]);
+          o.w = pack_bf16(v[6], v[7]);
+          *cp = o;
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmO, box, x, y);
+          bulk_commit();
+        }
       }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (lane == 0) bulk_wait<0>();
   }
   fence_before();
   cluster_sync_all();
@@ -593,9 +683,13 @@ int launch(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
 int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
                 const __nv_bfloat16 *residual, __nv_bfloat16 *out, int M, int N, int K, int epi,
                 cudaStream_t s) {
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, to, tr;
   LV_REQUIRE(make_map(&ta, A, M, K, 128), LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(A) failed");
   LV_REQUIRE(make_map(&tb, W, N, K, 128), LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(W) failed");
+  LV_REQUIRE(make_tma_2d_bf16(&to, out, N, M, (uint64_t)N * 2, 64, 32), LV_ERR_INTERNAL,
+             "cuTensorMapEncodeTiled(out) failed");
+  LV_REQUIRE(make_tma_2d_bf16(&tr, residual ? residual : out, N, M, (uint64_t)N * 2, 64, 32),
+             LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(residual) failed");
   static bool attr_set = false;
   if (!attr_set) {
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel,
@@ -604,8 +698,7 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bia
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = std::min(tiles, tc_gemm_num_sms() / 2);
-  tc_gemm_pair_kernel<<<2 * pairs, kThreads, kSmem2, s>>>(ta, tb, M, N, K, bias, residual, out,
-                                                          epi);
+  tc_gemm_pair_kernel<<<2 * pairs, kThreads, kSmem2, s>>>(ta, tb, to, tr, M, N, K, bias, epi);
   note_launch();
   LV_CHECK_CUDA(cudaGetLastError());
   return LV_OK;
