@@ -39,7 +39,7 @@ cudaError_t f32_gemm(const float *A, const float *W, const float *bias, const fl
 // each), out [T][H*dh]; bidirectional softmax(q k^T / sqrt(dh)) v per sequence.
 cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S,
                            int H, int dh, cudaStream_t s);
-extern int g_attn_mode;  // 0 auto (tcgen05 kernel for dh 64, S 128/256), 1 mma.sync kernel
+extern int g_attn_mode;  // see lv_set_attention_mode (leann_b200.h)
 cudaError_t attention_f32(const float *qkv, float *out, int n_seqs, int S, int H, int dh,
                           cudaStream_t s);
 
