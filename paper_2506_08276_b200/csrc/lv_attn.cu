@@ -194,7 +194,6 @@ __global__ void __launch_bounds__(256, DH == 64 ? 2 : 1) attn_bf16_kernel(const 
 // No mask (every passage is exactly S tokens) and no online rescaling (a row
 // of scores fits in TMEM). Batch-invariant: each item is a fixed-order
 // computation independent of the launch.
-constexpr int kAttnPolyDefault = 4;  // every 4th exponential on the FMA pipe
 namespace atc {
 constexpr int kThreads = 64 + 8 * 32;
 template <int S>
@@ -213,21 +212,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// 2^x for x <= 0 on the FMA/ALU pipes (offloads the MUFU pipe, the softmax's
-// bottleneck): x = j + f with j = rint(x) (magic-number rounding), 2^f from a
-// degree-3 least-squares polynomial on [-0.5, 0.5] (max relative error
-// 1.8e-4, below the 2^-9 half-ulp of the bf16 P it feeds), 2^j added to the
-// exponent field.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -125.f);
-  const float t = x + 12582912.f;  // 1.5 * 2^23
-  const float j = t - 12582912.f;
-  const float f = x - j;
-  const float p = fmaf(fmaf(fmaf(0.05460262f, f, 0.24192413f), f, 0.69331648f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
-template <int S, int kPolyEvery>
+template <int S>
 __global__ void __launch_bounds__(atc::kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out,
                    int n_items, int H, float scale_log2) {
@@ -333,55 +318,35 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
       const uint32_t ph = (uint32_t)(j >> 1) & 1;
       mbar_wait(&s_full[g], ph);
       fence_after();
-      // pass 1: row max. TMEM loads run one chunk ahead of the compute and the
-      // max is kept in 4 independent chains (2 warps per SMSP leave little
-      // latency hiding otherwise).
-      constexpr float kC = 0.18033688011112042f;  // log2(e) / sqrt(64)
-      float m4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
-      {
-        uint32_t ra[32], rb[32];
-        tmem_ld32_nowait(tb, ra);
+      // pass 1: row max
+      float mx = -FLT_MAX;
+#pragma unroll 1
+      for (int c = 0; c < S / 32; c += 2) {
+        uint32_t r0[32], r1[32];
+        tmem_ld32_nowait(tb + 32 * c, r0);
+        tmem_ld32_nowait(tb + 32 * c + 32, r1);
+        tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < S / 32; ++c) {
-          tmem_ld_wait();
-          uint32_t(&cur)[32] = (c & 1) ? rb : ra;
-          uint32_t(&nxt)[32] = (c & 1) ? ra : rb;
-          if (c + 1 < S / 32) tmem_ld32_nowait(tb + 32 * (c + 1), nxt);
-#pragma unroll
-          for (int e = 0; e < 32; ++e) m4[e & 3] = fmaxf(m4[e & 3], __uint_as_float(cur[e]));
-        }
+        for (int e = 0; e < 32; ++e)
+          mx = fmaxf(mx, fmaxf(__uint_as_float(r0[e]), __uint_as_float(r1[e])));
       }
-      const float mc = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * kC;
-      // pass 2: p = 2^(s*c - max*c) on the MUFU pipe, row sum (4 chains), P
-      // packed to bf16 and written over the consumed score columns
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
-      {
-        uint32_t ra[32], rb[32];
-        tmem_ld32_nowait(tb, ra);
+      const float mc = mx * scale_log2;
+      // pass 2: p = 2^(s*c - max*c), row sum, P (bf16) over the consumed columns
+      float sum = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < S / 32; ++c) {
+        uint32_t r0[32];
+        tmem_ld32(tb + 32 * c, r0);
+        uint32_t w[16];
 #pragma unroll
-        for (int c = 0; c < S / 32; ++c) {
-          tmem_ld_wait();
-          uint32_t(&cur)[32] = (c & 1) ? rb : ra;
-          uint32_t(&nxt)[32] = (c & 1) ? ra : rb;
-          if (c + 1 < S / 32) tmem_ld32_nowait(tb + 32 * (c + 1), nxt);
-          uint32_t w[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float x0 = fmaf(__uint_as_float(cur[2 * e]), kC, -mc);
-            const float x1 = fmaf(__uint_as_float(cur[2 * e + 1]), kC, -mc);
-            const float p0 = (kPolyEvery && (2 * e) % kPolyEvery == kPolyEvery - 1) ? ex2_poly(x0)
-                                                                                   : ex2_approx(x0);
-            const float p1 = (kPolyEvery && (2 * e + 1) % kPolyEvery == kPolyEvery - 1)
-                                 ? ex2_poly(x1)
-                                 : ex2_approx(x1);
-            s4[(2 * e) & 3] += p0;
-            s4[(2 * e + 1) & 3] += p1;
-            w[e] = pack_bf16(p0, p1);
-          }
-          tmem_st16(tb + 16 * c, w);
+        for (int e = 0; e < 16; ++e) {
+          const float p0 = ex2_approx(fmaf(__uint_as_float(r0[2 * e]), scale_log2, -mc));
+          const float p1 = ex2_approx(fmaf(__uint_as_float(r0[2 * e + 1]), scale_log2, -mc));
+          sum += p0 + p1;
+          w[e] = pack_bf16(p0, p1);
         }
+        tmem_st16(tb + 16 * c, w);
       }
-      const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
       tmem_st_wait();
       fence_before();
       __syncwarp();
@@ -430,7 +395,7 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
   }
 }
 
-template <int S, int P>
+template <int S>
 cudaError_t launch_attn_tc(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int H,
                            cudaStream_t s) {
   using C = atc::Cfg<S>;
@@ -440,31 +405,19 @@ cudaError_t launch_attn_tc(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<S, P>,
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<S>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int items = n_seqs * H;
   const int grid = std::min(items, tc_gemm_num_sms());
-  attn_tc_kernel<S, P><<<grid, atc::kThreads, C::kSmem, s>>>(tm, out, items, H, 0.f);
+  attn_tc_kernel<S><<<grid, atc::kThreads, C::kSmem, s>>>(tm, out, items, H,
+                                                          1.4426950408889634f / 8.0f);
   note_launch();
   return cudaGetLastError();
 }
 
-// tcgen05 attention variants: MUFU-only softmax, or every P-th exponential on
-// the FMA pipe (ex2_poly)
-template <int S>
-cudaError_t attn_tc_dispatch(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int H,
-                             int mode, cudaStream_t s) {
-  switch (mode) {
-    case 2: return launch_attn_tc<S, 0>(qkv, out, n_seqs, H, s);
-    case 3: return launch_attn_tc<S, 4>(qkv, out, n_seqs, H, s);
-    case 4: return launch_attn_tc<S, 3>(qkv, out, n_seqs, H, s);
-    case 5: return launch_attn_tc<S, 2>(qkv, out, n_seqs, H, s);
-    default: return launch_attn_tc<S, kAttnPolyDefault>(qkv, out, n_seqs, H, s);
-  }
-}
 
 // fp32 reference-order attention: one warp per (sequence, head, query row).
 __global__ void attn_f32_kernel(const float *__restrict__ qkv, float *__restrict__ out, int n_seqs,
@@ -521,8 +474,8 @@ cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
   if (S % 64 != 0 || dh % 16 != 0) return cudaErrorInvalidValue;
   if (g_attn_mode != 1 && dh == 64 && (S == 128 || S == 256)) {
     if (((uintptr_t)qkv & 15) != 0 || ((uintptr_t)out & 15) != 0) return cudaErrorInvalidValue;
-    return S == 256 ? attn_tc_dispatch<256>(qkv, out, n_seqs, H, g_attn_mode, s)
-                    : attn_tc_dispatch<128>(qkv, out, n_seqs, H, g_attn_mode, s);
+    return S == 256 ? launch_attn_tc<256>(qkv, out, n_seqs, H, s)
+                    : launch_attn_tc<128>(qkv, out, n_seqs, H, s);
   }
   const size_t smem = (size_t)3 * S * (dh + 8) * 2;
   const int threads = std::min(256, std::max(32, (S / 16) * 32));
