@@ -184,6 +184,9 @@ int lv_encode(lv_encoder *enc, const void *tokens, int32_t token_bytes, int64_t 
 int lv_encoder_profile(lv_encoder *enc, int enable);
 int lv_encoder_stats(lv_encoder *enc, lv_encoder_stats_t *stats);
 int lv_encoder_reset_stats(lv_encoder *enc);
+/* bf16 encoder: 1 = LayerNorms folded into the GEMM epilogues (default when
+ * hidden, ffn % 256 == 0), 0 = standalone LayerNorm kernels. */
+int lv_encoder_set_fused_ln(lv_encoder *enc, int enable);
 
 /* out[M][N] = epi(A[M][K] . W[N][K]^T (+ bias) ...), bf16 device pointers, fp32 bias;
  * epi: 0 bias, 1 bias + erf-GELU, 2 bias + residual. N % 128 == 0, K % 64 == 0. */

@@ -98,6 +98,7 @@ EXPORTS = {
     "lv_encoder_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "lv_set_gemm_mode": (C.c_int, [C.c_int]),
     "lv_set_attention_mode": (C.c_int, [C.c_int]),
+    "lv_encoder_set_fused_ln": (C.c_int, [C.c_void_p, C.c_int]),
     "lv_attention_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_int32, C.c_void_p]),
     "lv_encoder_stats": (C.c_int, [C.c_void_p, C.POINTER(EncoderStats)]),

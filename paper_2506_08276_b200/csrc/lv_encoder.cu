@@ -245,6 +245,66 @@ __global__ void pool_kernel(const T *__restrict__ x, float *__restrict__ out, in
   for (int c = threadIdx.x; c < d; c += blockDim.x) out[seq * d + c] = mv[nv++] * inv;
 }
 
+// Row LayerNorm statistics from the per-64-column-box (mean, M2) partials the
+// GEMM epilogue wrote (EPF_STATS): Chan's parallel combination in a fixed
+// order, population variance like the LayerNorm kernels, one thread per row.
+__global__ void ln_stats_finalize_kernel(const float2 *__restrict__ parts, int nbox,
+                                         float2 *__restrict__ out, int64_t rows) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const float2 *p = parts + r * nbox;
+  float m[32];
+  float mean = 0.f, m2 = 0.f;
+  for (int b = 0; b < nbox; ++b) {
+    const float2 t = __ldg(p + b);
+    m[b] = t.x;
+    mean += t.x;
+    m2 += t.y;
+  }
+  mean /= (float)nbox;
+  for (int b = 0; b < nbox; ++b) {
+    const float dm = m[b] - mean;
+    m2 = fmaf(64.f * dm, dm, m2);
+  }
+  out[r] = make_float2(mean, rsqrtf(m2 / (64.f * nbox) + kLnEps));
+}
+
+// pool_kernel over LN(y): mean_p LN(y_p) = g * mean_p((y_p - mu_p) * rstd_p) + b,
+// then L2 normalisation. One block per sequence.
+__global__ void pool_ln_kernel(const __nv_bfloat16 *__restrict__ y, const float2 *__restrict__ st,
+                               const float *__restrict__ g, const float *__restrict__ b,
+                               float *__restrict__ out, int S, int d) {
+  __shared__ float red[32];
+  __shared__ float2 sst[512];
+  const int64_t seq = blockIdx.x;
+  const __nv_bfloat16 *base = y + seq * S * d;
+  for (int p = threadIdx.x; p < S; p += blockDim.x) sst[p] = st[seq * S + p];
+  __syncthreads();
+  float local = 0.f;
+  float mv[4];
+  int nv = 0;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < S; ++p)
+      acc = fmaf(__bfloat162float(base[(size_t)p * d + c]) - sst[p].x, sst[p].y, acc);
+    const float v = fmaf(g[c], acc / (float)S, b[c]);
+    mv[nv++] = v;
+    local += v * v;
+  }
+  local = warp_sum(local);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = 1.0f / fmaxf(sqrtf(red[0]), 1e-12f);
+  nv = 0;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) out[seq * d + c] = mv[nv++] * inv;
+}
+
 // fp32 SIMT GEMM, 64x64 tile, 4x4 per thread; sequential fmaf over K.
 __global__ void __launch_bounds__(256)
     f32_gemm_kernel(const float *__restrict__ A, const float *__restrict__ W,
@@ -317,6 +377,11 @@ struct EncLayer {
   void *w_qkv = nullptr, *w_o = nullptr, *w_1 = nullptr, *w_2 = nullptr;
   float *b_qkv = nullptr, *b_o = nullptr, *b_1 = nullptr, *b_2 = nullptr;
   float *ln1_g = nullptr, *ln1_b = nullptr, *ln2_g = nullptr, *ln2_b = nullptr;
+  // LayerNorm folded into the consuming GEMM (bf16 fused mode): W' = W diag(gamma)
+  // (bf16), colc = W'.1, bias' = W.beta + b, for W_qkv (previous layer's LN2;
+  // layer >= 1) and W_1 (this layer's LN1)
+  void *w_qkv_f = nullptr, *w_1_f = nullptr;
+  float *c_qkv = nullptr, *e_qkv = nullptr, *c_1 = nullptr, *e_1 = nullptr;
 };
 
 struct lv_encoder {
@@ -328,6 +393,8 @@ struct lv_encoder {
   // activation workspace (element size 2 or 4), grown on demand
   int64_t cap_tokens = 0;
   void *x = nullptr, *qkv = nullptr, *ctx = nullptr, *y = nullptr, *h = nullptr;
+  float2 *st_part = nullptr, *st1 = nullptr, *st2 = nullptr;  // LN statistics (fused mode)
+  bool fuse_ln = false;  // bf16: LayerNorms folded into the GEMM epilogues
   // profiling of the dense GEMMs (lv_encoder_profile)
   bool profile = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -343,6 +410,9 @@ struct lv_encoder {
     cudaFree(ctx);
     cudaFree(y);
     cudaFree(h);
+    cudaFree(st_part);
+    cudaFree(st1);
+    cudaFree(st2);
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (auto &pr : ev_used) {
       cudaEventDestroy(pr.first);
@@ -354,6 +424,16 @@ struct lv_encoder {
 
 namespace lv {
 namespace {
+
+// round-to-nearest-even to bf16, kept in a float (host)
+float bf16_round_host(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return f;
+  u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
 
 int dev_alloc(lv_encoder *e, void **p, size_t bytes) {
   LV_CHECK_CUDA(cudaMalloc(p, bytes));
@@ -390,7 +470,11 @@ int ensure_ws(lv_encoder *e, int64_t tokens) {
   cudaFree(e->ctx);
   cudaFree(e->y);
   cudaFree(e->h);
+  cudaFree(e->st_part);
+  cudaFree(e->st1);
+  cudaFree(e->st2);
   e->x = e->qkv = e->ctx = e->y = e->h = nullptr;
+  e->st_part = e->st1 = e->st2 = nullptr;
   e->cap_tokens = 0;
   const size_t es = e->esize();
   const size_t d = e->cfg.hidden, ff = e->cfg.ffn;
@@ -399,6 +483,11 @@ int ensure_ws(lv_encoder *e, int64_t tokens) {
   LV_CHECK_CUDA(cudaMalloc(&e->ctx, tokens * d * es));
   LV_CHECK_CUDA(cudaMalloc(&e->y, tokens * d * es));
   LV_CHECK_CUDA(cudaMalloc(&e->h, tokens * ff * es));
+  if (e->cfg.precision == 1) {
+    LV_CHECK_CUDA(cudaMalloc(&e->st_part, tokens * (d / 64) * sizeof(float2)));
+    LV_CHECK_CUDA(cudaMalloc(&e->st1, tokens * sizeof(float2)));
+    LV_CHECK_CUDA(cudaMalloc(&e->st2, tokens * sizeof(float2)));
+  }
   e->cap_tokens = tokens;
   return LV_OK;
 }
@@ -438,6 +527,95 @@ int gemm(lv_encoder *e, const void *A, const void *W, const float *bias, const v
   return LV_OK;
 }
 
+// bf16 forward with the LayerNorms folded into the GEMM epilogues (x0 = the
+// embedding LN output is already in e->x). Per layer l (y2 of layer l-1 in x):
+//   qkv = LN2(y2).Wqkv + b        (l = 0: x0.Wqkv + b)            EPF_LN_IN
+//   y1  = ctx.Wo + bo + LN2(y2)   (l = 0: + x0), + row stats       EPF_RES[_LN] | EPF_STATS
+//   h   = gelu(LN1(y1).W1 + b1)                                    EPF_LN_IN | EPF_GELU
+//   y2  = h.W2 + b2 + LN1(y1), + row stats                         EPF_RES_LN | EPF_STATS
+// and the pooled output reads LN2(y2) through the statistics. No LayerNorm
+// output ever round-trips through HBM.
+int fused_gemm(lv_encoder *e, const void *A, const void *W, const void *res, void *out, int M,
+               int N, int K, const EpiParams &ep, cudaStream_t s) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (e->profile) {
+    e0 = take_event(e);
+    e1 = take_event(e);
+    cudaEventRecord(e0, s);
+  }
+  LV_TRY(tc_gemm_ex((const __nv_bfloat16 *)A, (const __nv_bfloat16 *)W,
+                    (const __nv_bfloat16 *)res, (__nv_bfloat16 *)out, M, N, K, ep, s));
+  if (e->profile) {
+    cudaEventRecord(e1, s);
+    e->ev_used.emplace_back(e0, e1);
+    e->ev_flops.push_back(2.0 * M * (double)N * K);
+  }
+  return LV_OK;
+}
+
+int finalize_stats(lv_encoder *e, float2 *dst, int M, cudaStream_t s) {
+  ln_stats_finalize_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(
+      e->st_part, e->cfg.hidden / 64, dst, M);
+  note_launch();
+  LV_CHECK_CUDA(cudaGetLastError());
+  return LV_OK;
+}
+
+int forward_fused(lv_encoder *e, int64_t ns, int S, int M, float *out, cudaStream_t s) {
+  const auto &c = e->cfg;
+  const int d = c.hidden, ff = c.ffn, H = c.heads, dh = c.hidden / c.heads;
+  using bf = __nv_bfloat16;
+  bf *x = (bf *)e->x, *qkv = (bf *)e->qkv, *ctx = (bf *)e->ctx, *y = (bf *)e->y, *h = (bf *)e->h;
+  for (size_t l = 0; l < e->layers.size(); ++l) {
+    const EncLayer &L = e->layers[l];
+    const EncLayer *P = l ? &e->layers[l - 1] : nullptr;
+    EpiParams q;
+    if (P) {
+      q.bias = L.e_qkv;
+      q.colc = L.c_qkv;
+      q.ln_in = e->st2;
+      q.flags = EPF_LN_IN;
+      LV_TRY(fused_gemm(e, x, L.w_qkv_f, nullptr, qkv, M, 3 * d, d, q, s));
+    } else {
+      q.bias = L.b_qkv;
+      LV_TRY(fused_gemm(e, x, L.w_qkv, nullptr, qkv, M, 3 * d, d, q, s));
+    }
+    LV_CHECK_CUDA(attention_bf16(qkv, ctx, (int)ns, S, H, dh, s));
+    EpiParams o;
+    o.bias = L.b_o;
+    o.flags = EPF_RES | EPF_STATS;
+    o.stats = e->st_part;
+    if (P) {
+      o.flags |= EPF_RES_LN;
+      o.res_ln = e->st2;
+      o.res_g = P->ln2_g;
+      o.res_b = P->ln2_b;
+    }
+    LV_TRY(fused_gemm(e, ctx, L.w_o, x, y, M, d, d, o, s));
+    LV_TRY(finalize_stats(e, e->st1, M, s));
+    EpiParams f1;
+    f1.bias = L.e_1;
+    f1.colc = L.c_1;
+    f1.ln_in = e->st1;
+    f1.flags = EPF_LN_IN | EPF_GELU;
+    LV_TRY(fused_gemm(e, y, L.w_1_f, nullptr, h, M, ff, d, f1, s));
+    EpiParams f2;
+    f2.bias = L.b_2;
+    f2.flags = EPF_RES | EPF_RES_LN | EPF_STATS;
+    f2.res_ln = e->st1;
+    f2.res_g = L.ln1_g;
+    f2.res_b = L.ln1_b;
+    f2.stats = e->st_part;
+    LV_TRY(fused_gemm(e, h, L.w_2, y, x, M, d, ff, f2, s));
+    LV_TRY(finalize_stats(e, e->st2, M, s));
+  }
+  const EncLayer &Z = e->layers.back();
+  pool_ln_kernel<<<(unsigned)ns, 256, 0, s>>>(x, e->st2, Z.ln2_g, Z.ln2_b, out, S, d);
+  note_launch();
+  LV_CHECK_CUDA(cudaGetLastError());
+  return LV_OK;
+}
+
 template <typename T>
 int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int32_t *d_ids,
             int64_t n_seqs, float *out, cudaStream_t s) {
@@ -455,6 +633,12 @@ int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int
         e->emb_b, d, x);
         note_launch();
     LV_CHECK_CUDA(cudaGetLastError());
+    if constexpr (sizeof(T) == 2) {
+      if (e->fuse_ln) {
+        LV_TRY(forward_fused(e, ns, S, M, out + s0 * d, s));
+        continue;
+      }
+    }
     for (const EncLayer &L : e->layers) {
       LV_TRY(gemm<T>(e, x, L.w_qkv, L.b_qkv, nullptr, qkv, M, 3 * d, d, EPI_BIAS, s));
       if constexpr (sizeof(T) == 2) {
@@ -564,6 +748,39 @@ int lv_encoder_create(const lv_encoder_config *cfg, const float *const *weights,
     up(&L.ln2_g, b + 10, d);
     up(&L.ln2_b, b + 11, d);
   }
+  // bf16: fold each LayerNorm into the GEMM that consumes it (see forward_fused)
+  if (rc == LV_OK && cfg->precision == 1 && d % 256 == 0 && ff % 256 == 0) {
+    std::vector<float> wf, cv, ev;
+    auto fold = [&](int wi, int bi, int gi, int be, size_t N, size_t K, void **wd, float **cd,
+                    float **ed) {
+      if (rc != LV_OK) return;
+      const float *W = weights[wi], *bias = weights[bi], *g = weights[gi], *beta = weights[be];
+      wf.resize(N * K);
+      cv.resize(N);
+      ev.resize(N);
+      for (size_t n = 0; n < N; ++n) {
+        double cs = 0.0, es = bias[n];
+        for (size_t k = 0; k < K; ++k) {
+          const float wr = bf16_round_host(W[n * K + k] * g[k]);
+          wf[n * K + k] = wr;
+          cs += wr;
+          es += (double)W[n * K + k] * beta[k];
+        }
+        cv[n] = (float)cs;
+        ev[n] = (float)es;
+      }
+      rc = upload_mat(e, wd, wf.data(), N * K);
+      if (rc == LV_OK) rc = upload_f32(e, cd, cv.data(), N);
+      if (rc == LV_OK) rc = upload_f32(e, ed, ev.data(), N);
+    };
+    for (int l = 0; l < cfg->layers; ++l) {
+      EncLayer &L = e->layers[l];
+      const int b = 4 + 12 * l;
+      if (l > 0) fold(b + 0, b + 1, b - 2, b - 1, 3 * d, d, &L.w_qkv_f, &L.c_qkv, &L.e_qkv);
+      fold(b + 6, b + 7, b + 4, b + 5, ff, d, &L.w_1_f, &L.c_1, &L.e_1);
+    }
+    e->fuse_ln = rc == LV_OK;
+  }
   if (rc != LV_OK) {
     delete e;
     return rc;
@@ -645,6 +862,15 @@ int lv_set_gemm_mode(int mode) {
   const int prev = g_gemm_mode;
   g_gemm_mode = mode;
   return prev;
+}
+
+int lv_encoder_set_fused_ln(lv_encoder *enc, int enable) {
+  LV_REQUIRE(enc, LV_ERR_USAGE, "null encoder");
+  const bool can = enc->cfg.precision == 1 && !enc->layers.empty() && enc->layers[0].w_1_f;
+  LV_REQUIRE(!enable || can, LV_ERR_USAGE,
+             "fused LayerNorm needs the bf16 encoder with hidden, ffn % 256 == 0");
+  enc->fuse_ln = enable != 0;
+  return LV_OK;
 }
 
 int lv_set_attention_mode(int mode) {

@@ -406,7 +406,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmO,
                         const __grid_constant__ CUtensorMap tmR, int M, int N, int K,
-                        const float *__restrict__ bias, int epi) {
+                        const EpiParams ep) {
   constexpr int BN = 256;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
@@ -520,7 +520,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;
     const int q = warp & 3;
     const int half = ew >> 2;
-    const bool has_res = epi == EPI_BIAS_RESIDUAL;
+    const int fl = ep.flags;
+    const bool has_res = (fl & EPF_RES) != 0;
     uint8_t *stg = sStage + ew * 2 * kBoxBytes;
     uint64_t *rb = rbar + 2 * ew;
     uint32_t rph = 0;  // parity bit per buffer
@@ -589,27 +590,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&rb[buf], (rph >> buf) & 1);
           rph ^= 1u << buf;
         }
-        const float4 *b4 = reinterpret_cast<const float4 *>(bias + x);
+        const int grow = y + lane;  // this thread's output row
+        const bool live = grow < M;
+        float mu_i = 0.f, rs_i = 1.f, mu_r = 0.f, rs_r = 1.f;
+        if ((fl & EPF_LN_IN) && live) {
+          const float2 t = __ldg(ep.ln_in + grow);
+          mu_i = t.x;
+          rs_i = t.y;
+        }
+        if ((fl & EPF_RES_LN) && live) {
+          const float2 t = __ldg(ep.res_ln + grow);
+          mu_r = t.x;
+          rs_r = t.y;
+        }
+        float sk = 0.f, s1 = 0.f, s2 = 0.f;  // shifted sums of the rounded outputs (EPF_STATS)
+        const float4 *b4 = reinterpret_cast<const float4 *>(ep.bias + x);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {  // 8 columns per 16-byte chunk
           const float4 bl = __ldg(b4 + 2 * c), bh = __ldg(b4 + 2 * c + 1);
-          float v[8] = {__uint_as_float(r[8 * c + 0]) + bl.x, __uint_as_float(r[8 * c + 1]) + bl.y,
-                        __uint_as_float(r[8 * c + 2]) + bl.z, __uint_as_float(r[8 * c + 3]) + bl.w,
-                        __uint_as_float(r[8 * c + 4]) + bh.x, __uint_as_float(r[8 * c + 5]) + bh.y,
-                        __uint_as_float(r[8 * c + 6]) + bh.z, __uint_as_float(r[8 * c + 7]) + bh.w};
+          const float bb[8] = {bl.x, bl.y, bl.z, bl.w, bh.x, bh.y, bh.z, bh.w};
+          float v[8];
+          if (fl & EPF_LN_IN) {
+            const float4 *c4 = reinterpret_cast<const float4 *>(ep.colc + x + 8 * c);
+            const float4 cl = __ldg(c4), ch = __ldg(c4 + 1);
+            const float cc[8] = {cl.x, cl.y, cl.z, cl.w, ch.x, ch.y, ch.z, ch.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              v[e] = fmaf(rs_i, fmaf(-mu_i, cc[e], __uint_as_float(r[8 * c + e])), bb[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[8 * c + e]) + bb[e];
+          }
           uint4 *cp = reinterpret_cast<uint4 *>(box + row_off + (((uint32_t)c ^ sw) << 4));
-          if (epi == EPI_BIAS_GELU) {
+          if (fl & EPF_GELU) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = gelu_erf(v[e]);
-          } else if (has_res) {
+          }
+          if (has_res) {
             const uint4 u = *cp;
             const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+            float rv[8];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f = __bfloat1622float2(h[e]);
-              v[2 * e] += f.x;
-              v[2 * e + 1] += f.y;
+              rv[2 * e] = f.x;
+              rv[2 * e + 1] = f.y;
             }
+            if (fl & EPF_RES_LN) {
+              const float4 *g4 = reinterpret_cast<const float4 *>(ep.res_g + x + 8 * c);
+              const float4 *e4 = reinterpret_cast<const float4 *>(ep.res_b + x + 8 * c);
+              const float4 gl = __ldg(g4), gh = __ldg(g4 + 1), el = __ldg(e4), eh = __ldg(e4 + 1);
+              const float gg[8] = {gl.x, gl.y, gl.z, gl.w, gh.x, gh.y, gh.z, gh.w};
+              const float be[8] = {el.x, el.y, el.z, el.w, eh.x, eh.y, eh.z, eh.w};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) rv[e] = fmaf((rv[e] - mu_r) * rs_r, gg[e], be[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] += rv[e];
           }
           uint4 o;
           o.x = pack_bf16(v[0], v[1]);
@@ -617,7 +654,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           o.z = pack_bf16(v[4], v[5]);
           o.w = pack_bf16(v[6], v[7]);
           *cp = o;
+          if (fl & EPF_STATS) {
+            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&o);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h[e]);
+              if (c == 0 && e == 0) sk = f.x;
+              const float a0 = f.x - sk, a1 = f.y - sk;
+              s1 += a0 + a1;
+              s2 = fmaf(a0, a0, fmaf(a1, a1, s2));
+            }
+          }
         }
+        if ((fl & EPF_STATS) && live)  // box (mean, M2) from sums shifted by its first value
+          ep.stats[(size_t)grow * (N / 64) + (x >> 6)] =
+              make_float2(sk + s1 * (1.f / 64.f), fmaxf(s2 - s1 * s1 * (1.f / 64.f), 0.f));
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -680,9 +731,8 @@ int launch(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
   return LV_OK;
 }
 
-int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
-                const __nv_bfloat16 *residual, __nv_bfloat16 *out, int M, int N, int K, int epi,
-                cudaStream_t s) {
+int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloat16 *residual,
+                __nv_bfloat16 *out, int M, int N, int K, const EpiParams &ep, cudaStream_t s) {
   CUtensorMap ta, tb, to, tr;
   LV_REQUIRE(make_map(&ta, A, M, K, 128), LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(A) failed");
   LV_REQUIRE(make_map(&tb, W, N, K, 128), LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(W) failed");
@@ -698,7 +748,7 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bia
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = std::min(tiles, tc_gemm_num_sms() / 2);
-  tc_gemm_pair_kernel<<<2 * pairs, kThreads, kSmem2, s>>>(ta, tb, to, tr, M, N, K, bias, epi);
+  tc_gemm_pair_kernel<<<2 * pairs, kThreads, kSmem2, s>>>(ta, tb, to, tr, M, N, K, ep);
   note_launch();
   LV_CHECK_CUDA(cudaGetLastError());
   return LV_OK;
@@ -733,6 +783,21 @@ int tc_gemm_num_sms() {
   return sms;
 }
 
+int tc_gemm_ex(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloat16 *residual,
+               __nv_bfloat16 *out, int M, int N, int K, const EpiParams &ep, cudaStream_t s) {
+  LV_REQUIRE(M >= 1 && N % 256 == 0 && K % kBK == 0 && K > 0, LV_ERR_USAGE,
+             "tc_gemm_ex: need N % 256 == 0 and K % 64 == 0");
+  LV_REQUIRE(ep.bias != nullptr, LV_ERR_USAGE, "tc_gemm_ex: bias required");
+  LV_REQUIRE(!(ep.flags & EPF_RES) || residual != nullptr, LV_ERR_USAGE,
+             "tc_gemm_ex: residual required");
+  LV_REQUIRE(!(ep.flags & EPF_LN_IN) || (ep.colc && ep.ln_in), LV_ERR_USAGE,
+             "tc_gemm_ex: LN-in needs colc and row statistics");
+  LV_REQUIRE(!(ep.flags & EPF_RES_LN) || (ep.res_ln && ep.res_g && ep.res_b), LV_ERR_USAGE,
+             "tc_gemm_ex: residual LN needs statistics and affine");
+  LV_REQUIRE(!(ep.flags & EPF_STATS) || ep.stats, LV_ERR_USAGE, "tc_gemm_ex: stats buffer");
+  return launch_pair(A, W, residual, out, M, N, K, ep, s);
+}
+
 int tc_gemm(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
             const __nv_bfloat16 *residual, __nv_bfloat16 *out, int M, int N, int K, int epi,
             cudaStream_t s) {
@@ -741,8 +806,12 @@ int tc_gemm(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
   LV_REQUIRE(bias != nullptr, LV_ERR_USAGE, "tc_gemm: bias required");
   LV_REQUIRE(epi != EPI_BIAS_RESIDUAL || residual != nullptr, LV_ERR_USAGE,
              "tc_gemm: residual required");
-  if (N % 256 == 0 && g_gemm_mode == 0)
-    return launch_pair(A, W, bias, residual, out, M, N, K, epi, s);
+  if (N % 256 == 0 && g_gemm_mode == 0) {
+    EpiParams ep;
+    ep.bias = bias;
+    ep.flags = epi == EPI_BIAS_GELU ? EPF_GELU : epi == EPI_BIAS_RESIDUAL ? EPF_RES : 0;
+    return launch_pair(A, W, residual, out, M, N, K, ep, s);
+  }
   if (N % 256 == 0) return launch<256>(A, W, bias, residual, out, M, N, K, epi, s);
   return launch<128>(A, W, bias, residual, out, M, N, K, epi, s);
 }

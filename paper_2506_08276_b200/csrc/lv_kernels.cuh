@@ -21,6 +21,32 @@ enum Epi : int {
 // K % 64 == 0, 16-byte aligned rows. Persistent, warp-specialised:
 // TMA producer / single-thread tcgen05.mma issuer / 4 epilogue warps.
 struct TcGemmPlan;  // cached tensor maps for one (A, W, M, N, K)
+
+// Generalised epilogue of the 2-CTA kernel (flags combine):
+//   v = acc + bias                                   (default)
+//   v = rstd_r * (acc - mean_r * colc) + bias        (EPF_LN_IN: A rows are raw
+//        pre-LayerNorm activations y and W was pre-scaled by the LN gamma, so
+//        W.LN(y) + b = rstd (W'.y - mean W'.1) + (W.beta + b) — the LayerNorm
+//        never materialises)
+//   v = gelu(v)                                      (EPF_GELU)
+//   v += res                                         (EPF_RES)
+//   v += (res - mean_r) * rstd_r * res_g + res_b     (EPF_RES | EPF_RES_LN)
+//   stats[row][col / 64] = (mean, M2) of the bf16-rounded outputs of each
+//        64-column box (EPF_STATS; combined by ln_stats_finalize)
+enum EpiFlag : int { EPF_GELU = 1, EPF_RES = 2, EPF_RES_LN = 4, EPF_LN_IN = 8, EPF_STATS = 16 };
+struct EpiParams {
+  const float *bias = nullptr;    // [N]
+  const float *colc = nullptr;    // [N]  EPF_LN_IN
+  const float2 *ln_in = nullptr;  // [M]  (mean, rstd) of the A rows, EPF_LN_IN
+  const float2 *res_ln = nullptr; // [M]  (mean, rstd) of the residual rows, EPF_RES_LN
+  const float *res_g = nullptr;   // [N]  EPF_RES_LN
+  const float *res_b = nullptr;   // [N]  EPF_RES_LN
+  float2 *stats = nullptr;        // [M][N / 64]  EPF_STATS
+  int flags = 0;
+};
+// 2-CTA kernel with the generalised epilogue; needs N % 256 == 0, K % 64 == 0.
+int tc_gemm_ex(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloat16 *residual,
+               __nv_bfloat16 *out, int M, int N, int K, const EpiParams &ep, cudaStream_t s);
 int tc_gemm(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
             const __nv_bfloat16 *residual, __nv_bfloat16 *out, int M, int N, int K, int epi,
             cudaStream_t s);

@@ -145,6 +145,11 @@ class GpuEncoder:
                                         res.ctypes.data, 0, None))
         return res
 
+    def set_fused_layernorm(self, enable: bool) -> None:
+        """bf16 mode: fold the LayerNorms into the GEMM epilogues (default) or
+        run them as standalone kernels."""
+        _lib.check(_lib.lib().lv_encoder_set_fused_ln(self.handle, 1 if enable else 0))
+
     # -- device-timed GEMM counters (roofline evidence)
     def profile(self, enable: bool = True) -> None:
         _lib.check(_lib.lib().lv_encoder_profile(self.handle, 1 if enable else 0))

@@ -93,6 +93,28 @@ def test_encoder_bert_base_bf16_close_to_torch(lv):
     assert cos.min() > 0.99, cos.min()
 
 
+@pytest.mark.parametrize("name", ["small", "bert-base"])
+def test_encoder_fused_layernorm_matches_unfused(lv, name):
+    """LayerNorms folded into the GEMM epilogues (row statistics from the
+    producing GEMM, gamma folded into the consuming weight) give the same
+    embeddings as standalone LayerNorm kernels up to bf16 rounding, and both
+    stay close to the fp32 torch oracle."""
+    from oracle.encoder_ref import RefEncoder
+    from paper_2506_08276_b200.encoder import ENCODERS, GpuEncoder, init_weights, synthetic_tokens
+    cfg = _small_cfg(lv, layers=3) if name == "small" else ENCODERS["bert-base"]
+    w = init_weights(cfg, seed=21)
+    tok = synthetic_tokens(8, 256 if name != "small" else 128, cfg.vocab, seed=22)
+    enc = GpuEncoder(cfg, w, precision="bf16")
+    fused = enc.encode(tok)
+    enc.set_fused_layernorm(False)
+    plain = enc.encode(tok)
+    ref = RefEncoder(cfg, w).encode(tok)
+    cos = lambda a, b: (a * b).sum(1) / np.linalg.norm(a, axis=1) / np.linalg.norm(b, axis=1)
+    assert cos(fused, plain).min() > 0.998, cos(fused, plain).min()
+    assert cos(fused, ref).min() > 0.99, cos(fused, ref).min()
+    assert cos(fused, ref).mean() >= cos(plain, ref).mean() - 2e-3
+
+
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_encoder_batch_invariant(lv, precision):
     """embed_all split is value-neutral (test_vectors.py:145-152): bitwise."""
