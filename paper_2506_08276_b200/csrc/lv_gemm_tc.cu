@@ -247,14 +247,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 // arrive on the leader's barrier. Per SM this loads (128 + 128) x 64 x 2 bytes
 // per 128 x 256 x 64 MACs: 1.5x the MACs per L2 byte of the 1-CTA kernel,
 // whose 50%-busy tensor pipe was bound by TMA/L2 throughput.
-constexpr int kStages2 = 5;
+// Shared-memory budget per CTA (<= 227 KB): residual GEMMs double-buffer the
+// epilogue boxes (residual prefetch one box ahead) and keep 4 operand stages;
+// the others single-buffer the output box and keep 5.
+template <bool kRes>
+struct PairCfg;
 constexpr int kHalfBytes = 128 * kBK * 2;          // 16 KB: A or B half per stage
 constexpr int kStageBytes2 = 2 * kHalfBytes;        // per CTA
 // epilogue staging: per epilogue warp two [32 rows][64 cols] bf16 boxes (4 KB
 // each, 128-byte swizzle) — residual tile in (TMA load), output tile out (TMA store)
 constexpr int kBoxBytes = 32 * 64 * 2;
-constexpr int kStagingBytes = kEpiWarps * 2 * kBoxBytes;
-constexpr int kSmem2 = kStages2 * kStageBytes2 + kStagingBytes + 1024 + 256;
+// per epilogue warp, two boxes' column vectors (bias, colc, gamma, beta: 64 fp32 each)
+constexpr int kColVecBytes = 4 * 64 * 4;
+constexpr int kColVecTotal = kEpiWarps * 2 * kColVecBytes;
+template <bool kRes>
+struct PairCfg {
+  static constexpr int kStages = kRes ? 4 : 5;
+  static constexpr int kBufs = kRes ? 2 : 1;  // epilogue boxes per warp
+  static constexpr int kStagingBytes = kEpiWarps * kBufs * kBoxBytes;
+  static constexpr int kSmem = kStages * kStageBytes2 + kStagingBytes + kColVecTotal + 1024 + 256;
+};
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -401,6 +413,7 @@ __device__ __forceinline__ void epilogue_apply(const uint32_t (&r)[32], const Ep
   }
 }
 
+template <bool kRes>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
@@ -412,9 +425,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
+  constexpr int kStages2 = PairCfg<kRes>::kStages;
+  constexpr int kStagingBytes = PairCfg<kRes>::kStagingBytes;
   uint8_t *sB = smem + kStages2 * kHalfBytes;
   uint8_t *sStage = sB + kStages2 * kHalfBytes;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sStage + kStagingBytes);
+  float *sColVec = reinterpret_cast<float *>(sStage + kStagingBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sStage + kStagingBytes + kColVecTotal);
   uint64_t *empty = full + kStages2;
   uint64_t *tfull = empty + kStages2;
   uint64_t *tempty = tfull + 2;
@@ -521,8 +537,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int half = ew >> 2;
     const int fl = ep.flags;
-    const bool has_res = (fl & EPF_RES) != 0;
-    uint8_t *stg = sStage + ew * 2 * kBoxBytes;
+    constexpr bool has_res = kRes;
+    uint8_t *stg = sStage + ew * PairCfg<kRes>::kBufs * kBoxBytes;
     uint64_t *rb = rbar + 2 * ew;
     uint32_t rph = 0;  // parity bit per buffer
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
@@ -539,6 +555,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_expect_tx(&rb[0], kBoxBytes);
       tma_load_2d(stg, &tmR, &rb[0], x, y, pol_r);
     }
+    // column vectors of a box -> this warp's shared buffer, by cp.async (one
+    // box ahead; reading them with per-chunk global loads exposed an L2 round
+    // trip per 8 columns)
+    float *cvw = sColVec + ew * 2 * (kColVecBytes / 4);
+    auto load_colvecs = [&](int cbuf, int x) {
+      float *dst = cvw + cbuf * (kColVecBytes / 4);
+      const int l16 = lane & 15, hi = lane >> 4;
+      const float *v0 = hi ? ep.colc : ep.bias;
+      if (!hi || (fl & EPF_LN_IN))
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                         smem_u32(dst + hi * 64 + 4 * l16)),
+                     "l"(v0 + x + 4 * l16)
+                     : "memory");
+      if (fl & EPF_RES_LN) {
+        const float *v1 = hi ? ep.res_b : ep.res_g;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                         smem_u32(dst + (2 + hi) * 64 + 4 * l16)),
+                     "l"(v1 + x + 4 * l16)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (pair < num_tiles) {
+      int x, y;
+      box_coords(pair, 0, x, y);
+      load_colvecs(0, x);
+    }
     // 16-byte chunk c of row r of a 128-byte-swizzled box
     const uint32_t row_off = (uint32_t)lane * 128;
     const uint32_t sw = (uint32_t)(lane & 7);
@@ -550,10 +593,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       fence_after();
 #pragma unroll 1
       for (int b = 0; b < 2; ++b, ++blk) {
-        const int buf = blk & 1;
-        uint8_t *box = stg + buf * kBoxBytes;
+        const int buf = blk & 1;  // column-vector buffer (and box buffer if double-buffered)
+        uint8_t *box = stg + (kRes ? buf * kBoxBytes : 0);
         int x, y;
         box_coords(tile, b, x, y);
+        const int grow = y + lane;  // this thread's output row
+        const bool live = grow < M;
+        float mu_i = 0.f, rs_i = 1.f, mu_r = 0.f, rs_r = 1.f;
+        if ((fl & EPF_LN_IN) && live) {
+          const float2 t = __ldg(ep.ln_in + grow);
+          mu_i = t.x;
+          rs_i = t.y;
+        }
+        if ((fl & EPF_RES_LN) && live) {
+          const float2 t = __ldg(ep.res_ln + grow);
+          mu_r = t.x;
+          rs_r = t.y;
+        }
+        {  // next box's column vectors into the other buffer
+          const int nt = b == 0 ? tile : tile + n_pairs;
+          if (nt < num_tiles) {
+            int nx, ny;
+            box_coords(nt, b ^ 1, nx, ny);
+            load_colvecs(buf ^ 1, nx);
+          } else {
+            asm volatile("cp.async.commit_group;" ::: "memory");
+          }
+        }
         uint32_t r[64];
         {
           uint32_t(&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
@@ -582,7 +648,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tma_load_2d(stg + (buf ^ 1) * kBoxBytes, &tmR, &rb[buf ^ 1], nx, ny, pol_r);
             }
           } else {
-            bulk_wait_read<1>();  // the store issued from this buffer two boxes ago
+            bulk_wait_read<0>();  // the previous box's store has read the (single) buffer
           }
         }
         __syncwarp();
@@ -590,29 +656,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&rb[buf], (rph >> buf) & 1);
           rph ^= 1u << buf;
         }
-        const int grow = y + lane;  // this thread's output row
-        const bool live = grow < M;
-        float mu_i = 0.f, rs_i = 1.f, mu_r = 0.f, rs_r = 1.f;
-        if ((fl & EPF_LN_IN) && live) {
-          const float2 t = __ldg(ep.ln_in + grow);
-          mu_i = t.x;
-          rs_i = t.y;
-        }
-        if ((fl & EPF_RES_LN) && live) {
-          const float2 t = __ldg(ep.res_ln + grow);
-          mu_r = t.x;
-          rs_r = t.y;
-        }
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // this box's column vectors
+        __syncwarp();
+        const float *cv = cvw + buf * (kColVecBytes / 4);
         float sk = 0.f, s1 = 0.f, s2 = 0.f;  // shifted sums of the rounded outputs (EPF_STATS)
-        const float4 *b4 = reinterpret_cast<const float4 *>(ep.bias + x);
+        const float4 *b4 = reinterpret_cast<const float4 *>(cv);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {  // 8 columns per 16-byte chunk
-          const float4 bl = __ldg(b4 + 2 * c), bh = __ldg(b4 + 2 * c + 1);
+          const float4 bl = b4[2 * c], bh = b4[2 * c + 1];
           const float bb[8] = {bl.x, bl.y, bl.z, bl.w, bh.x, bh.y, bh.z, bh.w};
           float v[8];
           if (fl & EPF_LN_IN) {
-            const float4 *c4 = reinterpret_cast<const float4 *>(ep.colc + x + 8 * c);
-            const float4 cl = __ldg(c4), ch = __ldg(c4 + 1);
+            const float4 *c4 = reinterpret_cast<const float4 *>(cv + 64 + 8 * c);
+            const float4 cl = c4[0], ch = c4[1];
             const float cc[8] = {cl.x, cl.y, cl.z, cl.w, ch.x, ch.y, ch.z, ch.w};
 #pragma unroll
             for (int e = 0; e < 8; ++e)
@@ -637,9 +693,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               rv[2 * e + 1] = f.y;
             }
             if (fl & EPF_RES_LN) {
-              const float4 *g4 = reinterpret_cast<const float4 *>(ep.res_g + x + 8 * c);
-              const float4 *e4 = reinterpret_cast<const float4 *>(ep.res_b + x + 8 * c);
-              const float4 gl = __ldg(g4), gh = __ldg(g4 + 1), el = __ldg(e4), eh = __ldg(e4 + 1);
+              const float4 *g4 = reinterpret_cast<const float4 *>(cv + 128 + 8 * c);
+              const float4 *e4 = reinterpret_cast<const float4 *>(cv + 192 + 8 * c);
+              const float4 gl = g4[0], gh = g4[1], el = e4[0], eh = e4[1];
               const float gg[8] = {gl.x, gl.y, gl.z, gl.w, gh.x, gh.y, gh.z, gh.w};
               const float be[8] = {el.x, el.y, el.z, el.w, eh.x, eh.y, eh.z, eh.w};
 #pragma unroll
@@ -742,13 +798,22 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
              LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(residual) failed");
   static bool attr_set = false;
   if (!attr_set) {
-    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
+    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PairCfg<false>::kSmem));
+    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PairCfg<true>::kSmem));
     attr_set = true;
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = std::min(tiles, tc_gemm_num_sms() / 2);
-  tc_gemm_pair_kernel<<<2 * pairs, kThreads, kSmem2, s>>>(ta, tb, to, tr, M, N, K, ep);
+  if (ep.flags & EPF_RES)
+    tc_gemm_pair_kernel<true><<<2 * pairs, kThreads, PairCfg<true>::kSmem, s>>>(ta, tb, to, tr, M,
+                                                                              N, K, ep);
+  else
+    tc_gemm_pair_kernel<false><<<2 * pairs, kThreads, PairCfg<false>::kSmem, s>>>(ta, tb, to, tr,
+                                                                                M, N, K, ep);
   note_launch();
   LV_CHECK_CUDA(cudaGetLastError());
   return LV_OK;

@@ -1,21 +1,33 @@
-"""Summarise an ncu --csv launch list (gpu__time_duration.sum) by kernel name."""
+"""Summarise an ncu --csv launch list by kernel: device time share, average
+time, DRAM bytes per launch and achieved DRAM GB/s (metrics
+gpu__time_duration.sum [, dram__bytes_read.sum, dram__bytes_write.sum]).
+Optional second argument: skip the first N launches (warm-up)."""
 import collections
 import csv
 import sys
+
+UNITS = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3,
+         "s": 1e6, "second": 1e6, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+         "KB": 1e3, "MB": 1e6, "GB": 1e9}
 rows = list(csv.reader(open(sys.argv[1])))
+skip = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[hi]
-ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-agg = collections.defaultdict(lambda: [0, 0.0])
+ki, ii, mi, vi, ui = (hdr.index(k) for k in ("Kernel Name", "ID", "Metric Name", "Metric Value",
+                                             "Metric Unit"))
+agg = collections.defaultdict(lambda: collections.defaultdict(float))
+launches = collections.defaultdict(set)
 for r in rows[hi + 1:]:
-    if len(r) <= vi:
+    if len(r) <= vi or int(r[ii]) < skip:
         continue
-    v = float(r[vi].replace(",", ""))
-    v *= {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "nsecond": 1}.get(r[ui], 1)
-    name = r[ki].split("(")[0][:70]
-    agg[name][0] += 1
-    agg[name][1] += v
-tot = sum(v[1] for v in agg.values())
-print(f"total {tot / 1e6:.3f} ms over {sum(v[0] for v in agg.values())} launches")
-for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
-    print(f"{v[1] / tot * 100:6.2f}%  {v[1] / 1e6:8.3f} ms  n={v[0]:5d}  avg={v[1] / v[0] / 1e3:8.1f} us  {k}")
+    v = float(r[vi].replace(",", "")) * UNITS.get(r[ui], 1.0)
+    name = r[ki].split("(")[0][:60]
+    agg[name][r[mi]] += v
+    launches[name].add(r[ii])
+tot = sum(a["gpu__time_duration.sum"] for a in agg.values())
+print(f"total {tot / 1e3:.3f} ms over {sum(len(v) for v in launches.values())} launches")
+for name, a in sorted(agg.items(), key=lambda x: -x[1]["gpu__time_duration.sum"]):
+    t, n = a["gpu__time_duration.sum"], len(launches[name])
+    b = a.get("dram__bytes_read.sum", 0.0) + a.get("dram__bytes_write.sum", 0.0)
+    print(f"{100 * t / tot:6.2f}%  {t / 1e3:9.3f} ms  n={n:5d}  avg={t / n:9.1f} us  "
+          f"dram/launch={b / n / 1e6:8.1f} MB  {b / t / 1e3 if t else 0:6.0f} GB/s  {name}")
