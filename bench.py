@@ -75,6 +75,19 @@ def load_peaks():
     return dict(FALLBACK_PEAKS), "fallback"
 
 
+def load_traffic():
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
+    the step's kernels, from the committed ncu launch-list summary
+    (profiles/traffic.json, written by tools/summarize_launches.py --json)."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        return {k: {"bytes_per_launch": v["dram_bytes_per_launch"], "source": d.get("source")}
+                for k, v in d["kernels"].items()}
+    except Exception:
+        return {}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -477,22 +490,40 @@ def main():
     if rank != 0:
         return
     # ---- rooflines
+    frontier_gbs = adc_bytes / (frontier_ms / 1e3) / 1e9 if frontier_ms else 0.0
+    traffic = load_traffic()
     gemm_tflops = est["gemm_flops"] / (est["gemm_ms"] / 1e3) / 1e12 if est["gemm_ms"] else 0.0
     gemm_peak = peaks["bf16_tflops_sustained"]
-    frontier_gbs = adc_bytes / (frontier_ms / 1e3) / 1e9 if frontier_ms else 0.0
-    roofline = {"kernel": "tc_gemm_kernel (encoder GEMMs, tcgen05/TMEM/TMA)", "bound": "tensor",
+    nl = max(1, est["gemm_launches"])
+    roofline = {"kernel": "tc_gemm_pair_kernel (encoder GEMMs, tcgen05 cta_group::2/TMEM/TMA, "
+                          "fused bias/GELU/residual/LayerNorm epilogues)", "bound": "tensor",
                 "achieved": round(gemm_tflops, 1), "peak": gemm_peak, "unit": "TFLOP/s",
-                "frac": round(gemm_tflops / gemm_peak, 4), "traffic": None,
+                "frac": round(gemm_tflops / gemm_peak, 4),
+                "traffic": traffic.get("tc_gemm_pair_kernel"),
                 "peak_source": f"{peaks_kind} bf16 sustained",
-                "launches": est["gemm_launches"],
-                "flops_per_launch": est["gemm_flops"] / max(1, est["gemm_launches"]),
+                "launches": est["gemm_launches"], "flops_per_launch": est["gemm_flops"] / nl,
+                "algorithmic_bytes_per_launch": est["gemm_bytes"] / nl,
                 "share_of_step": round(est["gemm_ms"] / ms, 4) if ms else None}
-    rooflines = [roofline, {
+    rooflines = [roofline]
+    if est["attn_ms"]:
+        na = max(1, est["attn_launches"])
+        attn_gbs = est["attn_bytes"] / (est["attn_ms"] / 1e3) / 1e9
+        rooflines.append({
+            "kernel": "attn_tc_kernel (tcgen05 Q.K^T -> TMEM softmax -> P.V)", "bound": "hbm",
+            "achieved": round(attn_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(attn_gbs / peaks["hbm_gbs"], 4),
+            "traffic": traffic.get("attn_tc_kernel"), "peak_source": peaks_kind,
+            "algorithmic_bytes_per_launch": est["attn_bytes"] / na,
+            "tensor_tflops": round(est["attn_flops"] / (est["attn_ms"] / 1e3) / 1e12, 1),
+            "launches": est["attn_launches"],
+            "share_of_step": round(est["attn_ms"] / ms, 4) if ms else None})
+    rooflines.append({
         "kernel": "frontier_kernel (CSR gather + ADC + AQ/EQ + exact scoring)", "bound": "hbm",
         "achieved": round(frontier_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-        "frac": round(frontier_gbs / peaks["hbm_gbs"], 4), "traffic": None,
+        "frac": round(frontier_gbs / peaks["hbm_gbs"], 4),
+        "traffic": traffic.get("frontier_kernel"),
         "peak_source": peaks_kind, "algorithmic_bytes": adc_bytes,
-        "share_of_step": round(frontier_ms / ms, 4) if ms else None}]
+        "share_of_step": round(frontier_ms / ms, 4) if ms else None})
     line = {
         "metric": "queries/sec at recall@3>=90% and recomputed embeddings/sec",
         "value": round(qps, 3), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -513,6 +544,7 @@ def main():
         "recomputes_per_query": round(recomputes_all / total_q, 2),
         "cache_hits_per_query": round(cache_hits * world / total_q, 2),
         "encoder_share": round(enc_ms / ms, 4) if ms else None,
+        "encoder_tflops_effective": round(physical_all * flops_pp / secs / 1e12, 1),
         "frontier_iterations": iters,
         "roofline": roofline, "rooflines": rooflines,
         "clocks": clocks, "gpu_launches": launches_all, "e2e": e2e,

@@ -136,6 +136,11 @@ typedef struct {
   int64_t gemm_launches;  /* timed GEMM launches (profile mode) */
   double gemm_ms;         /* summed CUDA-event time of those launches */
   double gemm_flops;      /* 2*M*N*K summed over those launches */
+  double gemm_bytes;      /* algorithmic bytes: A + W + out (+ residual) */
+  int64_t attn_launches;  /* timed attention launches (profile mode) */
+  double attn_ms;
+  double attn_flops;      /* 4*S^2*dh*H per sequence */
+  double attn_bytes;      /* qkv read + context written */
 } lv_encoder_stats_t;
 
 typedef struct {

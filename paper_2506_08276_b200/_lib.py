@@ -68,7 +68,9 @@ class EncoderConfigC(C.Structure):
 class EncoderStats(C.Structure):
     _fields_ = [
         ("passages", C.c_int64), ("gemm_launches", C.c_int64),
-        ("gemm_ms", C.c_double), ("gemm_flops", C.c_double),
+        ("gemm_ms", C.c_double), ("gemm_flops", C.c_double), ("gemm_bytes", C.c_double),
+        ("attn_launches", C.c_int64), ("attn_ms", C.c_double), ("attn_flops", C.c_double),
+        ("attn_bytes", C.c_double),
     ]
 
 

@@ -399,7 +399,11 @@ struct lv_encoder {
   bool profile = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used;
-  std::vector<double> ev_flops;
+  std::vector<double> ev_flops, ev_bytes;  // algorithmic work of each timed launch
+  std::vector<int> ev_kind;                // 0 GEMM, 1 attention
+  double gemm_bytes = 0.0;
+  int64_t attn_launches = 0;
+  double attn_ms = 0.0, attn_flops = 0.0, attn_bytes = 0.0;
   double gemm_ms = 0.0, gemm_flops = 0.0;
   int64_t gemm_launches = 0;
   int64_t passages = 0;
@@ -523,6 +527,9 @@ int gemm(lv_encoder *e, const void *A, const void *W, const float *bias, const v
     cudaEventRecord(e1, s);
     e->ev_used.emplace_back(e0, e1);
     e->ev_flops.push_back(2.0 * M * (double)N * K);
+    e->ev_bytes.push_back((double)sizeof(T) *
+                          ((double)M * K + (double)N * K + (double)M * N * (res ? 2 : 1)));
+    e->ev_kind.push_back(0);
   }
   return LV_OK;
 }
@@ -549,6 +556,30 @@ int fused_gemm(lv_encoder *e, const void *A, const void *W, const void *res, voi
     cudaEventRecord(e1, s);
     e->ev_used.emplace_back(e0, e1);
     e->ev_flops.push_back(2.0 * M * (double)N * K);
+    e->ev_bytes.push_back(2.0 * ((double)M * K + (double)N * K +
+                                 (double)M * N * ((ep.flags & EPF_RES) ? 2 : 1)));
+    e->ev_kind.push_back(0);
+  }
+  return LV_OK;
+}
+
+// bf16 attention with optional CUDA-event timing (profile mode): algorithmic
+// work 4*S^2*dh*H FLOPs and qkv + context bytes per sequence
+int timed_attention(lv_encoder *e, const __nv_bfloat16 *qkv, __nv_bfloat16 *ctx, int ns, int S,
+                    int H, int dh, cudaStream_t s) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (e->profile) {
+    e0 = take_event(e);
+    e1 = take_event(e);
+    cudaEventRecord(e0, s);
+  }
+  LV_CHECK_CUDA(attention_bf16(qkv, ctx, ns, S, H, dh, s));
+  if (e->profile) {
+    cudaEventRecord(e1, s);
+    e->ev_used.emplace_back(e0, e1);
+    e->ev_flops.push_back(4.0 * ns * (double)S * S * dh * H);
+    e->ev_bytes.push_back(2.0 * ns * (double)S * 4 * H * dh);
+    e->ev_kind.push_back(1);
   }
   return LV_OK;
 }
@@ -580,7 +611,7 @@ int forward_fused(lv_encoder *e, int64_t ns, int S, int M, float *out, cudaStrea
       q.bias = L.b_qkv;
       LV_TRY(fused_gemm(e, x, L.w_qkv, nullptr, qkv, M, 3 * d, d, q, s));
     }
-    LV_CHECK_CUDA(attention_bf16(qkv, ctx, (int)ns, S, H, dh, s));
+    LV_TRY(timed_attention(e, qkv, ctx, (int)ns, S, H, dh, s));
     EpiParams o;
     o.bias = L.b_o;
     o.flags = EPF_RES | EPF_STATS;
@@ -642,8 +673,8 @@ int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int
     for (const EncLayer &L : e->layers) {
       LV_TRY(gemm<T>(e, x, L.w_qkv, L.b_qkv, nullptr, qkv, M, 3 * d, d, EPI_BIAS, s));
       if constexpr (sizeof(T) == 2) {
-        LV_CHECK_CUDA(attention_bf16((const __nv_bfloat16 *)qkv, (__nv_bfloat16 *)ctx, (int)ns, S,
-                                     H, dh, s));
+        LV_TRY(timed_attention(e, (const __nv_bfloat16 *)qkv, (__nv_bfloat16 *)ctx, (int)ns, S,
+                               H, dh, s));
       } else {
         LV_CHECK_CUDA(attention_f32((const float *)qkv, (float *)ctx, (int)ns, S, H, dh, s));
       }
@@ -681,15 +712,25 @@ void encoder_collect_profile(lv_encoder *enc) {
   for (size_t i = 0; i < enc->ev_used.size(); ++i) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, enc->ev_used[i].first, enc->ev_used[i].second) == cudaSuccess) {
-      enc->gemm_ms += ms;
-      enc->gemm_flops += enc->ev_flops[i];
-      enc->gemm_launches += 1;
+      if (enc->ev_kind[i] == 0) {
+        enc->gemm_ms += ms;
+        enc->gemm_flops += enc->ev_flops[i];
+        enc->gemm_bytes += enc->ev_bytes[i];
+        enc->gemm_launches += 1;
+      } else {
+        enc->attn_ms += ms;
+        enc->attn_flops += enc->ev_flops[i];
+        enc->attn_bytes += enc->ev_bytes[i];
+        enc->attn_launches += 1;
+      }
     }
     enc->ev_pool.push_back(enc->ev_used[i].first);
     enc->ev_pool.push_back(enc->ev_used[i].second);
   }
   enc->ev_used.clear();
   enc->ev_flops.clear();
+  enc->ev_bytes.clear();
+  enc->ev_kind.clear();
 }
 
 }  // namespace lv
@@ -894,6 +935,11 @@ int lv_encoder_stats(lv_encoder *enc, lv_encoder_stats_t *st) {
   st->gemm_launches = enc->gemm_launches;
   st->gemm_ms = enc->gemm_ms;
   st->gemm_flops = enc->gemm_flops;
+  st->gemm_bytes = enc->gemm_bytes;
+  st->attn_launches = enc->attn_launches;
+  st->attn_ms = enc->attn_ms;
+  st->attn_flops = enc->attn_flops;
+  st->attn_bytes = enc->attn_bytes;
   return LV_OK;
 }
 
@@ -906,6 +952,9 @@ int lv_encoder_reset_stats(lv_encoder *enc) {
   enc->gemm_launches = 0;
   enc->gemm_ms = 0.0;
   enc->gemm_flops = 0.0;
+  enc->gemm_bytes = 0.0;
+  enc->attn_launches = 0;
+  enc->attn_ms = enc->attn_flops = enc->attn_bytes = 0.0;
   return LV_OK;
 }
 

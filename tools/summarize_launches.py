@@ -1,7 +1,9 @@
 """Summarise an ncu --csv launch list by kernel: device time share, average
 time, DRAM bytes per launch and achieved DRAM GB/s (metrics
 gpu__time_duration.sum [, dram__bytes_read.sum, dram__bytes_write.sum]).
-Optional second argument: skip the first N launches (warm-up)."""
+Optional second argument: skip the first N launches (warm-up); --json OUT
+writes per-kernel DRAM bytes per launch (bench.py reads profiles/traffic.json)."""
+import json
 import collections
 import csv
 import sys
@@ -9,8 +11,13 @@ import sys
 UNITS = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3,
          "s": 1e6, "second": 1e6, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
          "KB": 1e3, "MB": 1e6, "GB": 1e9}
-rows = list(csv.reader(open(sys.argv[1])))
-skip = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+args = [a for a in sys.argv[1:]]
+jout = None
+if "--json" in args:
+    jout = args[args.index("--json") + 1]
+    del args[args.index("--json"):args.index("--json") + 2]
+rows = list(csv.reader(open(args[0])))
+skip = int(args[1]) if len(args) > 1 else 0
 hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[hi]
 ki, ii, mi, vi, ui = (hdr.index(k) for k in ("Kernel Name", "ID", "Metric Name", "Metric Value",
@@ -31,3 +38,13 @@ for name, a in sorted(agg.items(), key=lambda x: -x[1]["gpu__time_duration.sum"]
     b = a.get("dram__bytes_read.sum", 0.0) + a.get("dram__bytes_write.sum", 0.0)
     print(f"{100 * t / tot:6.2f}%  {t / 1e3:9.3f} ms  n={n:5d}  avg={t / n:9.1f} us  "
           f"dram/launch={b / n / 1e6:8.1f} MB  {b / t / 1e3 if t else 0:6.0f} GB/s  {name}")
+
+if jout:
+    ker = {}
+    for name, a in agg.items():
+        short = name.split("::")[-1].split("<")[0].strip()
+        n = len(launches[name])
+        b = a.get("dram__bytes_read.sum", 0.0) + a.get("dram__bytes_write.sum", 0.0)
+        ker[short] = {"launches": n, "avg_us": a["gpu__time_duration.sum"] / n,
+                      "dram_bytes_per_launch": b / n}
+    json.dump({"source": args[0], "kernels": ker}, open(jout, "w"), indent=1)
