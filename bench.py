@@ -52,6 +52,15 @@ CONFIGS = {
                         "graph (M=32, m=6, beta=2%), PQ m=64, 4096-query pool, top-3",
                n=1_000_000, seq=256, encoder="bert-base", pq_m=64, k=3, n_queries=4096,
                batch=4096, corpus="lda"),
+    # config-4 (not the headline): Qwen3-Embedding-0.6B-shaped decoder encoder
+    # (arch 1, 481 GFLOP/passage), top-10, recompute-ratio sweep; use --n to
+    # bound the corpus (embedding 1M x 512-token passages takes ~10 min)
+    "c4": dict(workload="config-4: 1M passages x 512 tokens (LDA-style topic mixtures), "
+                        "Qwen3-Embedding-0.6B-shaped random-init encoder (1024-d, 28 layers, "
+                        "GQA 16/8 x 128, SwiGLU, RoPE, causal, last-token pool), top-10, "
+                        "recompute ratio 5-30%", n=1_000_000, seq=512, encoder="qwen3-0.6b",
+               pq_m=None, k=10, n_queries=1024, batch=1024, corpus="lda",
+               alphas="5,10,20,30"),
 }
 
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -82,7 +91,8 @@ def load_traffic():
     p = ROOT / "profiles" / "traffic.json"
     try:
         d = json.loads(p.read_text())
-        return {k: {"bytes_per_launch": v["dram_bytes_per_launch"], "source": d.get("source")}
+        return {k: {"bytes_per_launch": v["dram_bytes_per_launch"], "source": d.get("source"),
+                    "ratio_to_algorithmic": v.get("ratio_to_algorithmic")}
                 for k, v in d["kernels"].items()}
     except Exception:
         return {}
@@ -154,8 +164,9 @@ def setup(cfg, args, device):
     qtokens = gen(max(cfg["n_queries"], args.pool), args.seed + 1)
     weights = init_weights(ecfg, seed=args.seed + 2)
     enc = GpuEncoder(ecfg, weights, precision="bf16", device=device)
-    tok_dev = torch.from_numpy(tokens.view(np.int16)).cuda(device)
-    qtok_dev = torch.from_numpy(qtokens.view(np.int16)).cuda(device)
+    iview = np.int16 if tokens.dtype == np.uint16 else np.int32
+    tok_dev = torch.from_numpy(tokens.view(iview)).cuda(device)
+    qtok_dev = torch.from_numpy(qtokens.view(iview)).cuda(device)
     log(f"tokens ready {time.time() - t0:.1f}s")
     t1 = time.time()
     E = enc.encode(tok_dev)
@@ -297,7 +308,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="queries per rank per step")
     ap.add_argument("--ef", type=int, default=0, help="skip tune_ef and use this ef")
     ap.add_argument("--ef-max", type=int, default=512)
-    ap.add_argument("--alphas", default="30,50,70,80,90,100",
+    ap.add_argument("--alphas", default="",
                     help="rerank percents tried by the tuner (the first is used with --ef)")
     ap.add_argument("--corpus", default="", choices=["", "lda", "uniform"])
     ap.add_argument("--inflight", type=int, default=0, help="concurrent query slots per rank")
@@ -311,9 +322,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.pool = 0
-    args.alphas = [float(x) for x in args.alphas.split(",")]
-    args.alpha = args.alphas[0]
     cfg = dict(CONFIGS[args.config])
+    args.alphas = [float(x) for x in (args.alphas or cfg.get("alphas", "30,50,70,80,90,100")).split(",")]
+    args.alpha = args.alphas[0]
     args.pool = (args.batch or cfg["batch"]) * int(os.environ.get("WORLD_SIZE", "1"))
     if args.n:
         cfg["n"] = args.n
@@ -461,7 +472,8 @@ def main():
                                  rerank_percent=args.alpha, cache_percent=args.cache_percent)
         e2e_steps = min(args.steps, 2)   # bounds the run time; same step definition
         pinned = [torch.from_numpy(np.ascontiguousarray(
-            W["qtokens"][query_slice(args.warmup + s)]).view(np.int16)).pin_memory()
+            W["qtokens"][query_slice(args.warmup + s)]).view(
+            np.int16 if W["qtokens"].dtype == np.uint16 else np.int32)).pin_memory()
             for s in range(e2e_steps)]
         searcher.search(pinned[0].cuda(), top_k=k, complexity=ef)  # warm
         barrier()

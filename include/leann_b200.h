@@ -144,14 +144,20 @@ typedef struct {
 } lv_encoder_stats_t;
 
 typedef struct {
-  int32_t arch;         /* 0 = BERT-style post-LN GELU, mean pool (C1-C3) */
+  int32_t arch;         /* 0 = BERT-style post-LN GELU, mean pool (C1-C3);
+                           1 = decoder-style (Qwen3-shaped, C4): pre-RMSNorm, GQA with
+                           per-head q/k RMSNorm + RoPE, causal, SwiGLU, last-token pool */
   int32_t layers;
   int32_t hidden;
   int32_t heads;
   int32_t ffn;
   int32_t vocab;
   int32_t max_seq;
-  int32_t precision;    /* 0 = fp32 (parity mode), 1 = bf16 tcgen05 */
+  int32_t precision;    /* 0 = fp32 (parity mode), 1 = bf16 tcgen05 (arch 1: bf16 only) */
+  int32_t kv_heads;     /* arch 1: key/value heads (0 = heads) */
+  int32_t head_dim;     /* arch 1: per-head dimension (0 = hidden / heads) */
+  float rope_theta;     /* arch 1 */
+  float norm_eps;       /* arch 1: RMSNorm epsilon */
 } lv_encoder_config;
 
 const char *lv_last_error(void);
@@ -201,6 +207,12 @@ int lv_gemm_bf16(const void *A, const void *W, const float *bias, const void *re
  * qkv [n_seqs*S][3*H*dh] (q | k | v), out [n_seqs*S][H*dh]. S % 64 == 0, dh in {64, 128}. */
 int lv_attention_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int32_t H,
                       int32_t dh, void *stream);
+/* Grouped-query attention (decoder-style encoder, config-4), bf16 device
+ * pointers: qkv [n_seqs*S][(Hq + 2*Hkv)*dh] (q heads | k heads | v heads),
+ * out [n_seqs*S][Hq*dh]; causal != 0 masks keys after the query. S % 64 == 0,
+ * dh in {64, 128}, Hq % Hkv == 0. */
+int lv_attention_gqa_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int32_t Hq,
+                          int32_t Hkv, int32_t dh, int32_t causal, void *stream);
 /* GEMM kernel selection: 0 = auto (2-CTA cta_group::2 kernel when N % 256 == 0),
  * 1 = 1-CTA kernel only. Returns the previous mode. */
 int lv_set_gemm_mode(int mode);

@@ -61,7 +61,8 @@ class EncoderConfigC(C.Structure):
     _fields_ = [
         ("arch", C.c_int32), ("layers", C.c_int32), ("hidden", C.c_int32),
         ("heads", C.c_int32), ("ffn", C.c_int32), ("vocab", C.c_int32),
-        ("max_seq", C.c_int32), ("precision", C.c_int32),
+        ("max_seq", C.c_int32), ("precision", C.c_int32), ("kv_heads", C.c_int32),
+        ("head_dim", C.c_int32), ("rope_theta", C.c_float), ("norm_eps", C.c_float),
     ]
 
 
@@ -100,6 +101,8 @@ EXPORTS = {
     "lv_encoder_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "lv_set_gemm_mode": (C.c_int, [C.c_int]),
     "lv_set_attention_mode": (C.c_int, [C.c_int]),
+    "lv_attention_gqa_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "lv_encoder_set_fused_ln": (C.c_int, [C.c_void_p, C.c_int]),
     "lv_attention_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_int32, C.c_void_p]),

@@ -419,6 +419,171 @@ cudaError_t launch_attn_tc(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
 }
 
 
+// ---------------------------------------------------------------------------
+// attn_flash_kernel: grouped-query attention with an optional causal mask for
+// the decoder-style (Qwen3-shaped, config-4) encoder: q heads Hq, k/v heads
+// Hkv (q head h reads k/v head h / (Hq / Hkv)), head dim DH in {64, 128}, any
+// S % 64 == 0 (S = 512 at config-4 does not fit shared memory whole, so K/V
+// stream through a 2-stage cp.async ring of 64-key blocks with an online
+// softmax). Row layout of qkv: [q heads | k heads | v heads] x DH.
+// One CTA = 64 query rows of one (sequence, q head), 4 warps x 16 rows;
+// tensor-core math as attn_bf16_kernel (mma.sync m16n8k16, ldmatrix).
+template <int DH, bool CAUSAL>
+__global__ void __launch_bounds__(128) attn_flash_kernel(const __nv_bfloat16 *__restrict__ qkv,
+                                                         __nv_bfloat16 *__restrict__ out, int S,
+                                                         int Hq, int Hkv, float scale_log2) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int LD = DH + 8;
+  constexpr int kVec = DH / 8;
+  __nv_bfloat16 *Qs = reinterpret_cast<__nv_bfloat16 *>(smem);
+  __nv_bfloat16 *Ks = Qs + 64 * LD;       // [2][64][LD]
+  __nv_bfloat16 *Vs = Ks + 2 * 64 * LD;   // [2][64][LD]
+  const int qb = blockIdx.x;
+  const int seq = blockIdx.y / Hq, h = blockIdx.y % Hq, g = h / (Hq / Hkv);
+  const int RS = (Hq + 2 * Hkv) * DH;
+  const size_t row0 = (size_t)seq * S;
+  const __nv_bfloat16 *qbase = qkv + row0 * RS + h * DH;
+  const __nv_bfloat16 *kbase = qkv + row0 * RS + (Hq + g) * DH;
+  const __nv_bfloat16 *vbase = qkv + row0 * RS + (Hq + Hkv + g) * DH;
+  for (int i = threadIdx.x; i < 64 * kVec; i += blockDim.x) {
+    const int j = i / kVec, c = (i % kVec) * 8;
+    cp_async16(Qs + j * LD + c, qbase + (size_t)(qb * 64 + j) * RS + c);
+  }
+  auto load_kv = [&](int kb, int st) {
+    for (int i = threadIdx.x; i < 64 * kVec; i += blockDim.x) {
+      const int j = i / kVec, c = (i % kVec) * 8;
+      const size_t r = (size_t)(kb * 64 + j) * RS + c;
+      cp_async16(Ks + (st * 64 + j) * LD + c, kbase + r);
+      cp_async16(Vs + (st * 64 + j) * LD + c, vbase + r);
+    }
+  };
+  const int nkv = CAUSAL ? qb + 1 : S / 64;
+  load_kv(0, 0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, t = lane & 3;
+  const int lr = lane & 7, lm = lane >> 3;
+  const int r0 = warp * 16;                 // this warp's rows within the block
+  const int qrow0 = qb * 64 + r0 + gq;      // query index of accumulator rows c[0..1]
+  uint32_t qa[DH / 16][4];
+  float o[DH / 8][4];
+#pragma unroll
+  for (int i = 0; i < DH / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -FLT_MAX, m1 = -FLT_MAX, l0 = 0.f, l1 = 0.f;
+  for (int kb = 0; kb < nkv; ++kb) {
+    const int st = kb & 1;
+    if (kb + 1 < nkv) load_kv(kb + 1, st ^ 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    if (kb == 0) {
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks)
+        ldsm_x4(qa[ks], Qs + (r0 + (lane & 15)) * LD + ks * 16 + (lane >> 4) * 8);
+    }
+    const __nv_bfloat16 *Kb = Ks + st * 64 * LD, *Vb = Vs + st * 64 * LD;
+    float sc[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks) {
+        uint32_t b[4];
+        ldsm_x4(b, Kb + (np * 16 + (lm >> 1) * 8 + lr) * LD + ks * 16 + (lm & 1) * 8);
+        mma_bf16_16816(sc[2 * np], qa[ks], b[0], b[1]);
+        mma_bf16_16816(sc[2 * np + 1], qa[ks], b[2], b[3]);
+      }
+    }
+    if (CAUSAL && kb == qb) {  // diagonal block: key > query is masked
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const int key = kb * 64 + nt * 8 + 2 * t;
+        if (key > qrow0) sc[nt][0] = -INFINITY;
+        if (key + 1 > qrow0) sc[nt][1] = -INFINITY;
+        if (key > qrow0 + 8) sc[nt][2] = -INFINITY;
+        if (key + 1 > qrow0 + 8) sc[nt][3] = -INFINITY;
+      }
+    }
+    float mx0 = m0, mx1 = m1;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      mx0 = fmaxf(mx0, fmaxf(sc[nt][0], sc[nt][1]));
+      mx1 = fmaxf(mx1, fmaxf(sc[nt][2], sc[nt][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(kFull, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(kFull, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, 2));
+    const float c0 = exp2f((m0 - mx0) * scale_log2), c1 = exp2f((m1 - mx1) * scale_log2);
+    m0 = mx0;
+    m1 = mx1;
+    const float sm0 = mx0 * scale_log2, sm1 = mx1 * scale_log2;
+    l0 *= c0;
+    l1 *= c1;
+#pragma unroll
+    for (int i = 0; i < DH / 8; ++i) {
+      o[i][0] *= c0;
+      o[i][1] *= c0;
+      o[i][2] *= c1;
+      o[i][3] *= c1;
+    }
+    uint32_t pa[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = exp2f(fmaf(sc[nt][0], scale_log2, -sm0));
+      const float p1 = exp2f(fmaf(sc[nt][1], scale_log2, -sm0));
+      const float p2 = exp2f(fmaf(sc[nt][2], scale_log2, -sm1));
+      const float p3 = exp2f(fmaf(sc[nt][3], scale_log2, -sm1));
+      l0 += p0 + p1;
+      l1 += p2 + p3;
+      const int j = nt >> 1, hi = nt & 1;
+      pa[j][hi ? 2 : 0] = pack2(p0, p1);
+      pa[j][hi ? 3 : 1] = pack2(p2, p3);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int dp = 0; dp < DH / 16; ++dp) {
+        uint32_t b[4];
+        ldsm_x4_t(b, Vb + (j * 16 + (lm & 1) * 8 + lr) * LD + dp * 16 + (lm >> 1) * 8);
+        mma_bf16_16816(o[2 * dp], pa[j], b[0], b[1]);
+        mma_bf16_16816(o[2 * dp + 1], pa[j], b[2], b[3]);
+      }
+    }
+    __syncthreads();  // the next iteration's prefetch overwrites this stage
+  }
+  l0 += __shfl_xor_sync(kFull, l0, 1);
+  l0 += __shfl_xor_sync(kFull, l0, 2);
+  l1 += __shfl_xor_sync(kFull, l1, 1);
+  l1 += __shfl_xor_sync(kFull, l1, 2);
+  const float i0 = 1.f / l0, i1 = 1.f / l1;
+  const int D = Hq * DH;
+  __nv_bfloat16 *o0 = out + (row0 + qrow0) * D + h * DH;
+  __nv_bfloat16 *o1 = o0 + (size_t)8 * D;
+#pragma unroll
+  for (int nt = 0; nt < DH / 8; ++nt) {
+    *reinterpret_cast<uint32_t *>(o0 + nt * 8 + 2 * t) = pack2(o[nt][0] * i0, o[nt][1] * i0);
+    *reinterpret_cast<uint32_t *>(o1 + nt * 8 + 2 * t) = pack2(o[nt][2] * i1, o[nt][3] * i1);
+  }
+}
+
+template <int DH, bool CAUSAL>
+cudaError_t launch_flash(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S, int Hq,
+                         int Hkv, cudaStream_t s) {
+  const size_t smem = (size_t)5 * 64 * (DH + 8) * 2;
+  cudaError_t e = cudaFuncSetAttribute(attn_flash_kernel<DH, CAUSAL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(S / 64, n_seqs * Hq);
+  attn_flash_kernel<DH, CAUSAL><<<grid, 128, smem, s>>>(qkv, out, S, Hq, Hkv,
+                                                        1.4426950408889634f / sqrtf((float)DH));
+  note_launch();
+  return cudaGetLastError();
+}
+
+
 // fp32 reference-order attention: one warp per (sequence, head, query row).
 __global__ void attn_f32_kernel(const float *__restrict__ qkv, float *__restrict__ out, int n_seqs,
                                 int S, int H, int dh, float scale) {
@@ -497,6 +662,19 @@ cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
     return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+cudaError_t attention_gqa_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S,
+                               int Hq, int Hkv, int dh, bool causal, cudaStream_t s) {
+  if (n_seqs <= 0) return cudaSuccess;
+  if (S % 64 != 0 || Hkv <= 0 || Hq % Hkv != 0) return cudaErrorInvalidValue;
+  if (dh == 64)
+    return causal ? launch_flash<64, true>(qkv, out, n_seqs, S, Hq, Hkv, s)
+                  : launch_flash<64, false>(qkv, out, n_seqs, S, Hq, Hkv, s);
+  if (dh == 128)
+    return causal ? launch_flash<128, true>(qkv, out, n_seqs, S, Hq, Hkv, s)
+                  : launch_flash<128, false>(qkv, out, n_seqs, S, Hq, Hkv, s);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t attention_f32(const float *qkv, float *out, int n_seqs, int S, int H, int dh,

@@ -16,6 +16,7 @@
 //   against the torch fp32 oracle (oracle/encoder_ref.py).
 // Both are batch-invariant: a passage's embedding never depends on the batch
 // it rides in (the test_vectors.py:145-152 contract).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -305,6 +306,169 @@ __global__ void pool_ln_kernel(const __nv_bfloat16 *__restrict__ y, const float2
   for (int c = threadIdx.x; c < d; c += blockDim.x) out[seq * d + c] = mv[nv++] * inv;
 }
 
+// ---- decoder-style encoder (arch 1, Qwen3-shaped, config-4) kernels --------
+
+// x[row] = tok_emb[token of row] (fp32 table -> bf16), one warp per row.
+__global__ void embed_gather_kernel(const void *__restrict__ tokens, int token_bytes, int S,
+                                    const int32_t *__restrict__ ids, int64_t seq0, int64_t n_seqs,
+                                    const float *__restrict__ tok_emb, int vocab, int d,
+                                    __nv_bfloat16 *__restrict__ out) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_seqs * S) return;
+  const int64_t n = seq0 + row / S;
+  const int p = (int)(row % S);
+  const int64_t src = ids ? (int64_t)__ldg(ids + n) : n;
+  uint32_t tok = token_bytes == 2
+                     ? (uint32_t)__ldg(reinterpret_cast<const uint16_t *>(tokens) + src * S + p)
+                     : __ldg(reinterpret_cast<const uint32_t *>(tokens) + src * S + p);
+  if (tok >= (uint32_t)vocab) tok = vocab - 1;
+  const float4 *te = reinterpret_cast<const float4 *>(tok_emb + (size_t)tok * d);
+  uint2 *o = reinterpret_cast<uint2 *>(out + row * d);
+  for (int c = lane; c < d / 4; c += 32) {
+    const float4 v = __ldg(te + c);
+    uint2 u;
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    u.x = *reinterpret_cast<uint32_t *>(&a);
+    u.y = *reinterpret_cast<uint32_t *>(&b);
+    o[c] = u;
+  }
+}
+
+// out = x * rsqrt(mean(x^2) + eps) * g (RMSNorm), bf16 rows, one warp per row,
+// d % 256 == 0 (16-byte accesses).
+__global__ void rmsnorm_bf16_kernel(const __nv_bfloat16 *__restrict__ in,
+                                    __nv_bfloat16 *__restrict__ out, const float *__restrict__ g,
+                                    int64_t rows, int d, float eps) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const uint4 *x = reinterpret_cast<const uint4 *>(in + row * d);
+  const int nv = d / 256;
+  float v[4][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i >= nv) break;
+    const uint4 u = __ldg(x + i * 32 + lane);
+    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      v[i][2 * e] = f.x;
+      v[i][2 * e + 1] = f.y;
+      ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+    }
+  }
+  const float r = rsqrtf(warp_sum(ss) / d + eps);
+  uint4 *o = reinterpret_cast<uint4 *>(out + row * d);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i >= nv) break;
+    const int c0 = (i * 32 + lane) * 8;
+    uint4 u;
+    uint32_t *w = reinterpret_cast<uint32_t *>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 hh = __floats2bfloat162_rn(v[i][2 * e] * r * __ldg(g + c0 + 2 * e),
+                                                v[i][2 * e + 1] * r * __ldg(g + c0 + 2 * e + 1));
+      w[e] = *reinterpret_cast<uint32_t *>(&hh);
+    }
+    o[i * 32 + lane] = u;
+  }
+}
+
+// In place on the q and k heads of qkv rows: per-head RMSNorm (q_norm /
+// k_norm gammas) then rotary embedding (rotate-half convention, inv_freq_i =
+// theta^(-2i/dh), position = row % S). One warp per (row, head); dh/32
+// elements per lane, element j pairs with j + dh/2 inside the same lane.
+template <int DH>
+__global__ void qk_norm_rope_kernel(__nv_bfloat16 *__restrict__ qkv, int64_t rows, int S, int Hq,
+                                    int Hkv, const float *__restrict__ qg,
+                                    const float *__restrict__ kg, float eps, float theta) {
+  constexpr int E = DH / 32;
+  const int nh = Hq + Hkv;
+  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (item >= rows * nh) return;
+  const int64_t row = item / nh;
+  const int hd = (int)(item % nh);
+  const int p = (int)(row % S);
+  const float *g = hd < Hq ? qg : kg;
+  __nv_bfloat16 *x = qkv + row * (int64_t)(Hq + 2 * Hkv) * DH + hd * DH;
+  float v[E];
+  float ss = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    v[e] = __bfloat162float(x[e * 32 + lane]);
+    ss = fmaf(v[e], v[e], ss);
+  }
+  const float r = rsqrtf(warp_sum(ss) / DH + eps);
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] *= r * __ldg(g + e * 32 + lane);
+  float o[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = e * 32 + lane;
+    const int i = j % (DH / 2);
+    const float inv = powf(theta, -2.0f * (float)i / (float)DH);
+    float sn, cs;
+    sincosf((float)p * inv, &sn, &cs);
+    const int pe = e < E / 2 ? e + E / 2 : e - E / 2;  // partner j +- dh/2
+    const float rot = e < E / 2 ? -v[pe] : v[pe];
+    o[e] = fmaf(v[e], cs, rot * sn);
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e * 32 + lane] = __float2bfloat16_rn(o[e]);
+}
+
+// act[row][c] = silu(gu[row][c]) * gu[row][ff + c]   (gate | up halves)
+__global__ void silu_mul_kernel(const __nv_bfloat16 *__restrict__ gu, __nv_bfloat16 *__restrict__ act,
+                                int64_t rows, int ff) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // 8-element chunk
+  const int per = ff / 8;
+  if (i >= rows * per) return;
+  const int64_t row = i / per;
+  const int c = (int)(i % per) * 8;
+  const uint4 a = *reinterpret_cast<const uint4 *>(gu + row * 2 * ff + c);
+  const uint4 b = *reinterpret_cast<const uint4 *>(gu + row * 2 * ff + ff + c);
+  const __nv_bfloat162 *ha = reinterpret_cast<const __nv_bfloat162 *>(&a);
+  const __nv_bfloat162 *hb = reinterpret_cast<const __nv_bfloat162 *>(&b);
+  uint4 u;
+  uint32_t *w = reinterpret_cast<uint32_t *>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 fa = __bfloat1622float2(ha[e]), fb = __bfloat1622float2(hb[e]);
+    __nv_bfloat162 r = __floats2bfloat162_rn(fa.x / (1.f + __expf(-fa.x)) * fb.x,
+                                             fa.y / (1.f + __expf(-fa.y)) * fb.y);
+    w[e] = *reinterpret_cast<uint32_t *>(&r);
+  }
+  *reinterpret_cast<uint4 *>(act + row * ff + c) = u;
+}
+
+// Last-token pooling: final RMSNorm of row S-1 of each sequence, then L2
+// normalisation. One warp per sequence.
+__global__ void pool_last_kernel(const __nv_bfloat16 *__restrict__ x, const float *__restrict__ g,
+                                 float *__restrict__ out, int64_t n_seqs, int S, int d, float eps) {
+  const int64_t seq = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (seq >= n_seqs) return;
+  const __nv_bfloat16 *r = x + (seq * S + S - 1) * d;
+  float ss = 0.f;
+  for (int c = lane; c < d; c += 32) {
+    const float v = __bfloat162float(r[c]);
+    ss = fmaf(v, v, ss);
+  }
+  const float rn = rsqrtf(warp_sum(ss) / d + eps);
+  float nn = 0.f;
+  for (int c = lane; c < d; c += 32) {
+    const float v = __bfloat162float(r[c]) * rn * g[c];
+    nn = fmaf(v, v, nn);
+  }
+  const float inv = 1.0f / fmaxf(sqrtf(warp_sum(nn)), 1e-12f);
+  for (int c = lane; c < d; c += 32) out[seq * d + c] = __bfloat162float(r[c]) * rn * g[c] * inv;
+}
+
 // fp32 SIMT GEMM, 64x64 tile, 4x4 per thread; sequential fmaf over K.
 __global__ void __launch_bounds__(256)
     f32_gemm_kernel(const float *__restrict__ A, const float *__restrict__ W,
@@ -384,8 +548,17 @@ struct EncLayer {
   float *c_qkv = nullptr, *e_qkv = nullptr, *c_1 = nullptr, *e_1 = nullptr;
 };
 
+// decoder-style (arch 1) layer: pre-RMSNorm, GQA, SwiGLU
+struct DecLayer {
+  float *ln1_g = nullptr, *qn_g = nullptr, *kn_g = nullptr, *ln2_g = nullptr;
+  void *w_qkv = nullptr, *w_o = nullptr, *w_gu = nullptr /* [gate; up] */, *w_down = nullptr;
+};
+
 struct lv_encoder {
   lv_encoder_config cfg{};
+  std::vector<DecLayer> dec;           // arch 1
+  float *final_g = nullptr;            // arch 1 final RMSNorm
+  float *zeros = nullptr;              // arch 1: zero bias for bias-free projections
   int device = 0;
   float *tok_emb = nullptr, *pos_emb = nullptr, *emb_g = nullptr, *emb_b = nullptr;
   std::vector<EncLayer> layers;
@@ -482,11 +655,18 @@ int ensure_ws(lv_encoder *e, int64_t tokens) {
   e->cap_tokens = 0;
   const size_t es = e->esize();
   const size_t d = e->cfg.hidden, ff = e->cfg.ffn;
+  size_t w_qkv = 3 * d, w_ctx = d, w_h = ff;
+  if (e->cfg.arch == 1) {
+    const size_t dh = e->cfg.head_dim, hq = e->cfg.heads, hk = e->cfg.kv_heads;
+    w_qkv = std::max((hq + 2 * hk) * dh, ff);  // also holds the SwiGLU activation
+    w_ctx = hq * dh;
+    w_h = 2 * ff;
+  }
   LV_CHECK_CUDA(cudaMalloc(&e->x, tokens * d * es));
-  LV_CHECK_CUDA(cudaMalloc(&e->qkv, tokens * 3 * d * es));
-  LV_CHECK_CUDA(cudaMalloc(&e->ctx, tokens * d * es));
+  LV_CHECK_CUDA(cudaMalloc(&e->qkv, tokens * w_qkv * es));
+  LV_CHECK_CUDA(cudaMalloc(&e->ctx, tokens * w_ctx * es));
   LV_CHECK_CUDA(cudaMalloc(&e->y, tokens * d * es));
-  LV_CHECK_CUDA(cudaMalloc(&e->h, tokens * ff * es));
+  LV_CHECK_CUDA(cudaMalloc(&e->h, tokens * w_h * es));
   if (e->cfg.precision == 1) {
     LV_CHECK_CUDA(cudaMalloc(&e->st_part, tokens * (d / 64) * sizeof(float2)));
     LV_CHECK_CUDA(cudaMalloc(&e->st1, tokens * sizeof(float2)));
@@ -692,6 +872,64 @@ int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int
   return LV_OK;
 }
 
+// Decoder-style encoder (arch 1), bf16 only. Per layer (residual stream x):
+//   h = RMSNorm(x) ; qkv = h.Wqkv ; q, k <- RoPE(RMSNorm_head(q | k))
+//   x = x + GQA_causal(q, k, v).Wo ; h = RMSNorm(x)
+//   x = x + (silu(h.Wg) * (h.Wu)).Wd
+// out = normalize(RMSNorm_final(x[last token])).
+int forward_decoder(lv_encoder *e, const void *tokens, int token_bytes, int S,
+                    const int32_t *d_ids, int64_t n_seqs, float *out, cudaStream_t s) {
+  using bf = __nv_bfloat16;
+  const auto &c = e->cfg;
+  const int d = c.hidden, ff = c.ffn, Hq = c.heads, Hk = c.kv_heads, dh = c.head_dim;
+  const int nqkv = (Hq + 2 * Hk) * dh;
+  const int64_t max_tokens = std::max<int64_t>(S, (int64_t)1 << 18);
+  const int64_t chunk = std::max<int64_t>(1, max_tokens / S);
+  LV_TRY(ensure_ws(e, std::min<int64_t>(n_seqs, chunk) * S));
+  bf *cur = (bf *)e->x, *tmp = (bf *)e->y, *qkv = (bf *)e->qkv, *ctx = (bf *)e->ctx,
+     *gu = (bf *)e->h;
+  for (int64_t s0 = 0; s0 < n_seqs; s0 += chunk) {
+    const int64_t ns = std::min(chunk, n_seqs - s0);
+    const int M = (int)(ns * S);
+    cur = (bf *)e->x;
+    tmp = (bf *)e->y;
+    embed_gather_kernel<<<(unsigned)((M + 7) / 8), 256, 0, s>>>(
+        tokens, token_bytes, S, d_ids, s0, ns, e->tok_emb, c.vocab, d, cur);
+    note_launch();
+    const unsigned rn_blocks = (unsigned)((M + 7) / 8);
+    for (const DecLayer &L : e->dec) {
+      rmsnorm_bf16_kernel<<<rn_blocks, 256, 0, s>>>(cur, tmp, L.ln1_g, M, d, c.norm_eps);
+      note_launch();
+      LV_TRY(gemm<bf>(e, tmp, L.w_qkv, e->zeros, nullptr, qkv, M, nqkv, d, EPI_BIAS, s));
+      const int64_t items = (int64_t)M * (Hq + Hk);
+      if (dh == 128)
+        qk_norm_rope_kernel<128><<<(unsigned)((items + 7) / 8), 256, 0, s>>>(
+            qkv, M, S, Hq, Hk, L.qn_g, L.kn_g, c.norm_eps, c.rope_theta);
+      else
+        qk_norm_rope_kernel<64><<<(unsigned)((items + 7) / 8), 256, 0, s>>>(
+            qkv, M, S, Hq, Hk, L.qn_g, L.kn_g, c.norm_eps, c.rope_theta);
+      note_launch();
+      LV_CHECK_CUDA(attention_gqa_bf16(qkv, ctx, (int)ns, S, Hq, Hk, dh, true, s));
+      LV_TRY(gemm<bf>(e, ctx, L.w_o, e->zeros, cur, tmp, M, d, Hq * dh, EPI_BIAS_RESIDUAL, s));
+      std::swap(cur, tmp);
+      rmsnorm_bf16_kernel<<<rn_blocks, 256, 0, s>>>(cur, tmp, L.ln2_g, M, d, c.norm_eps);
+      note_launch();
+      LV_TRY(gemm<bf>(e, tmp, L.w_gu, e->zeros, nullptr, gu, M, 2 * ff, d, EPI_BIAS, s));
+      const int64_t chunks = (int64_t)M * (ff / 8);
+      silu_mul_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, s>>>(gu, qkv, M, ff);
+      note_launch();
+      LV_TRY(gemm<bf>(e, qkv, L.w_down, e->zeros, cur, tmp, M, d, ff, EPI_BIAS_RESIDUAL, s));
+      std::swap(cur, tmp);
+    }
+    pool_last_kernel<<<(unsigned)((ns + 7) / 8), 256, 0, s>>>(cur, e->final_g, out + s0 * d, ns, S,
+                                                              d, c.norm_eps);
+    note_launch();
+    LV_CHECK_CUDA(cudaGetLastError());
+  }
+  e->passages += n_seqs;
+  return LV_OK;
+}
+
 }  // namespace
 
 int encoder_hidden(const lv_encoder *enc) { return enc ? enc->cfg.hidden : 0; }
@@ -701,6 +939,8 @@ int encode_node_rows(lv_encoder *enc, const void *tokens, int token_bytes, int s
   LV_REQUIRE(enc, LV_ERR_USAGE, "null encoder");
   LV_REQUIRE(seq_len <= enc->cfg.max_seq, LV_ERR_USAGE, "seq_len exceeds the encoder's max_seq");
   if (count <= 0) return LV_OK;
+  if (enc->cfg.arch == 1)
+    return forward_decoder(enc, tokens, token_bytes, seq_len, d_ids, count, out, s);
   if (enc->cfg.precision == 1)
     return forward<__nv_bfloat16>(enc, tokens, token_bytes, seq_len, d_ids, count, out, s);
   return forward<float>(enc, tokens, token_bytes, seq_len, d_ids, count, out, s);
@@ -735,13 +975,79 @@ void encoder_collect_profile(lv_encoder *enc) {
 
 }  // namespace lv
 
+namespace {
+int create_decoder(const lv_encoder_config *cfg_in, const float *const *weights, int32_t n_weights,
+                   int device, lv_encoder **out) {
+  lv_encoder_config cfg = *cfg_in;
+  if (cfg.kv_heads <= 0) cfg.kv_heads = cfg.heads;
+  if (cfg.head_dim <= 0) cfg.head_dim = cfg.heads ? cfg.hidden / cfg.heads : 0;
+  if (cfg.norm_eps <= 0.f) cfg.norm_eps = 1e-6f;
+  if (cfg.rope_theta <= 0.f) cfg.rope_theta = 1e6f;
+  LV_REQUIRE(cfg.precision == 1, LV_ERR_USAGE, "the decoder-style encoder (arch 1) is bf16 only");
+  LV_REQUIRE(cfg.layers >= 1 && cfg.heads >= 1 && cfg.kv_heads >= 1 &&
+                 cfg.heads % cfg.kv_heads == 0 && (cfg.head_dim == 64 || cfg.head_dim == 128),
+             LV_ERR_USAGE, "arch 1: need heads % kv_heads == 0 and head_dim in {64, 128}");
+  const int nqkv = (cfg.heads + 2 * cfg.kv_heads) * cfg.head_dim;
+  LV_REQUIRE(cfg.hidden % 256 == 0 && cfg.hidden <= 1024 && cfg.ffn % 256 == 0 && nqkv % 256 == 0 &&
+                 (cfg.heads * cfg.head_dim) % 64 == 0,
+             LV_ERR_USAGE, "arch 1: hidden, ffn, (heads + 2 kv_heads) * head_dim % 256 == 0");
+  LV_REQUIRE(cfg.vocab >= 1 && cfg.max_seq >= 1 && cfg.max_seq <= 4096, LV_ERR_USAGE,
+             "bad encoder geometry");
+  LV_REQUIRE(n_weights == 2 + 9 * cfg.layers, LV_ERR_USAGE,
+             "arch 1 weights: expected 2 + 9 * layers arrays");
+  DeviceGuard guard(device);
+  auto *e = new lv_encoder();
+  e->cfg = cfg;
+  e->device = device;
+  const size_t d = cfg.hidden, ff = cfg.ffn, dh = cfg.head_dim, hq = cfg.heads;
+  int rc = LV_OK;
+  auto up = [&](float **dst, int idx, size_t n) {
+    if (rc == LV_OK) rc = upload_f32(e, dst, weights[idx], n);
+  };
+  auto upm = [&](void **dst, int idx, size_t n) {
+    if (rc == LV_OK) rc = upload_mat(e, dst, weights[idx], n);
+  };
+  up(&e->tok_emb, 0, (size_t)cfg.vocab * d);
+  e->dec.resize(cfg.layers);
+  std::vector<float> gu;
+  for (int l = 0; l < cfg.layers && rc == LV_OK; ++l) {
+    DecLayer &L = e->dec[l];
+    const int b = 1 + 9 * l;
+    up(&L.ln1_g, b + 0, d);
+    upm(&L.w_qkv, b + 1, (size_t)nqkv * d);
+    up(&L.qn_g, b + 2, dh);
+    up(&L.kn_g, b + 3, dh);
+    upm(&L.w_o, b + 4, d * hq * dh);
+    up(&L.ln2_g, b + 5, d);
+    gu.resize(2 * ff * d);  // [gate; up] stacked so one GEMM produces both
+    std::memcpy(gu.data(), weights[b + 6], ff * d * 4);
+    std::memcpy(gu.data() + ff * d, weights[b + 7], ff * d * 4);
+    if (rc == LV_OK) rc = upload_mat(e, &L.w_gu, gu.data(), 2 * ff * d);
+    upm(&L.w_down, b + 8, d * ff);
+  }
+  up(&e->final_g, 1 + 9 * cfg.layers, d);
+  if (rc == LV_OK) {
+    const size_t nz = std::max<size_t>(std::max<size_t>(nqkv, 2 * ff), d);
+    std::vector<float> z(nz, 0.f);
+    rc = upload_f32(e, &e->zeros, z.data(), nz);
+  }
+  if (rc != LV_OK) {
+    delete e;
+    return rc;
+  }
+  *out = e;
+  return LV_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int lv_encoder_create(const lv_encoder_config *cfg, const float *const *weights, int32_t n_weights,
                       int device, lv_encoder **out) {
   LV_REQUIRE(cfg && weights && out, LV_ERR_USAGE, "lv_encoder_create: null argument");
   *out = nullptr;
-  LV_REQUIRE(cfg->arch == 0, LV_ERR_USAGE, "only arch 0 (BERT-style) is supported");
+  LV_REQUIRE(cfg->arch == 0 || cfg->arch == 1, LV_ERR_USAGE, "arch must be 0 or 1");
+  if (cfg->arch == 1) return create_decoder(cfg, weights, n_weights, device, out);
   LV_REQUIRE(cfg->precision == 0 || cfg->precision == 1, LV_ERR_USAGE, "precision must be 0 or 1");
   LV_REQUIRE(cfg->layers >= 1 && cfg->heads >= 1 && cfg->hidden % cfg->heads == 0, LV_ERR_USAGE,
              "bad encoder geometry");
@@ -896,6 +1202,16 @@ int lv_attention_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int
              "lv_attention_bf16: need S % 64 == 0 and dh in {64, 128}");
   LV_CHECK_CUDA(attention_bf16((const __nv_bfloat16 *)qkv, (__nv_bfloat16 *)out, n_seqs, S, H, dh,
                                (cudaStream_t)stream));
+  return LV_OK;
+}
+
+int lv_attention_gqa_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int32_t Hq,
+                          int32_t Hkv, int32_t dh, int32_t causal, void *stream) {
+  LV_REQUIRE(qkv && out, LV_ERR_USAGE, "lv_attention_gqa_bf16: null argument");
+  LV_REQUIRE(S % 64 == 0 && (dh == 64 || dh == 128) && Hkv >= 1 && Hq % Hkv == 0, LV_ERR_USAGE,
+             "lv_attention_gqa_bf16: need S % 64 == 0, dh in {64, 128}, Hq % Hkv == 0");
+  LV_CHECK_CUDA(attention_gqa_bf16((const __nv_bfloat16 *)qkv, (__nv_bfloat16 *)out, n_seqs, S, Hq,
+                                   Hkv, dh, causal != 0, (cudaStream_t)stream));
   return LV_OK;
 }
 

@@ -65,6 +65,11 @@ cudaError_t f32_gemm(const float *A, const float *W, const float *bias, const fl
 // each), out [T][H*dh]; bidirectional softmax(q k^T / sqrt(dh)) v per sequence.
 cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S,
                            int H, int dh, cudaStream_t s);
+// grouped-query attention, optional causal mask (decoder-style encoder, config-4):
+// qkv [T][(Hq + 2 Hkv) * dh] = q heads | k heads | v heads, out [T][Hq * dh];
+// dh in {64, 128}, S % 64 == 0.
+cudaError_t attention_gqa_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S,
+                               int Hq, int Hkv, int dh, bool causal, cudaStream_t s);
 extern int g_attn_mode;  // see lv_set_attention_mode (leann_b200.h)
 cudaError_t attention_f32(const float *qkv, float *out, int n_seqs, int S, int H, int dh,
                           cudaStream_t s);

@@ -29,7 +29,10 @@ ITEMS_IDX = "items.idx"
 
 @dataclass(frozen=True)
 class EncoderConfig:
-    """Shape of a BERT-style (post-LN, erf-GELU, mean-pool + L2) encoder."""
+    """Encoder shape. arch 0: BERT-style (post-LN, erf-GELU, mean-pool + L2;
+    configs 1-3). arch 1: decoder-style, Qwen3-Embedding-shaped (pre-RMSNorm,
+    grouped-query attention with per-head q/k RMSNorm and RoPE, causal,
+    SwiGLU, final RMSNorm, last-token pool + L2; config 4)."""
 
     name: str
     layers: int
@@ -38,15 +41,29 @@ class EncoderConfig:
     ffn: int
     vocab: int
     max_seq: int
+    arch: int = 0
+    kv_heads: int = 0       # arch 1 (0 = heads)
+    head_dim: int = 0       # arch 1 (0 = hidden / heads)
+    rope_theta: float = 1e6
+    norm_eps: float = 1e-6
 
     @property
     def dim(self) -> int:
         return self.hidden
 
+    @property
+    def n_weights(self) -> int:
+        return 4 + 12 * self.layers if self.arch == 0 else 2 + 9 * self.layers
+
     def flops_per_passage(self, seq_len: int) -> float:
-        """Algorithmic FLOPs of one passage: GEMMs + attention matmuls."""
+        """Algorithmic FLOPs of one passage: GEMMs + attention
+        matmuls; causal attention counted at half."""
         d, f, S = self.hidden, self.ffn, seq_len
-        return float(self.layers * (2 * S * (4 * d * d + 2 * d * f) + 4 * S * S * d))
+        if self.arch == 0:
+            return float(self.layers * (2 * S * (4 * d * d + 2 * d * f) + 4 * S * S * d))
+        dh = self.head_dim or d // self.heads
+        dq, dkv = self.heads * dh, (self.kv_heads or self.heads) * dh
+        return float(self.layers * (2 * S * (d * 2 * dq + 2 * d * dkv + 3 * d * f) + 2 * S * S * dq))
 
 
 ENCODERS = {
@@ -54,15 +71,21 @@ ENCODERS = {
     "c1-4l-d256": EncoderConfig("c1-4l-d256", 4, 256, 4, 1024, 30522, 512),
     # configs 2/3: BERT-base / Contriever-shaped
     "bert-base": EncoderConfig("bert-base", 12, 768, 12, 3072, 30522, 512),
+    # config 4: Qwen3-Embedding-0.6B-shaped (28 layers, 1024 hidden, 16 q / 8 kv
+    # heads x 128, SwiGLU 3072, RoPE theta 1e6, RMSNorm eps 1e-6)
+    "qwen3-0.6b": EncoderConfig("qwen3-0.6b", 28, 1024, 16, 3072, 151669, 512, arch=1,
+                                kv_heads=8, head_dim=128),
 }
 
 PRECISIONS = {"fp32": 0, "bf16": 1}
 
 
 def init_weights(cfg: EncoderConfig, seed: int = 0) -> list[np.ndarray]:
-    """Seeded random init (PCG64), fp32, in the C-ABI order:
+    """Seeded random init (PCG64), fp32, in the C-ABI order. arch 0:
     tok_emb, pos_emb, emb_ln_g, emb_ln_b, then per layer
-    Wqkv, bqkv, Wo, bo, ln1_g, ln1_b, W1, b1, W2, b2, ln2_g, ln2_b."""
+    Wqkv, bqkv, Wo, bo, ln1_g, ln1_b, W1, b1, W2, b2, ln2_g, ln2_b.
+    arch 1: tok_emb, then per layer ln1_g, Wqkv (q | k | v heads), q_norm_g,
+    k_norm_g, Wo, ln2_g, W_gate, W_up, W_down, and a final norm_g."""
     rng = np.random.default_rng(seed)
     d, f = cfg.hidden, cfg.ffn
 
@@ -71,6 +94,16 @@ def init_weights(cfg: EncoderConfig, seed: int = 0) -> list[np.ndarray]:
 
     def gamma(n):
         return (1.0 + nrm(n)).astype(np.float32)
+
+    if cfg.arch == 1:
+        dh = cfg.head_dim or d // cfg.heads
+        hk = cfg.kv_heads or cfg.heads
+        w = [nrm(cfg.vocab, d)]
+        for _ in range(cfg.layers):
+            w += [gamma(d), nrm((cfg.heads + 2 * hk) * dh, d), gamma(dh), gamma(dh),
+                  nrm(d, cfg.heads * dh), gamma(d), nrm(f, d), nrm(f, d), nrm(d, f)]
+        w.append(gamma(d))
+        return w
 
     w = [nrm(cfg.vocab, d), nrm(cfg.max_seq, d), gamma(d), nrm(d)]
     for _ in range(cfg.layers):
@@ -92,13 +125,15 @@ class GpuEncoder:
         self.device = device
         if weights is None:
             weights = init_weights(cfg, seed)
-        if len(weights) != 4 + 12 * cfg.layers:
-            raise InvalidArgumentError("weights: expected 4 + 12 * layers arrays")
+        if len(weights) != cfg.n_weights:
+            raise InvalidArgumentError(f"weights: expected {cfg.n_weights} arrays")
         ws = [np.ascontiguousarray(x, dtype=np.float32) for x in weights]
         arr = (C.c_void_p * len(ws))(*[x.ctypes.data for x in ws])
         c = _lib.EncoderConfigC()
-        c.arch, c.layers, c.hidden, c.heads = 0, cfg.layers, cfg.hidden, cfg.heads
+        c.arch, c.layers, c.hidden, c.heads = cfg.arch, cfg.layers, cfg.hidden, cfg.heads
         c.ffn, c.vocab, c.max_seq, c.precision = cfg.ffn, cfg.vocab, cfg.max_seq, PRECISIONS[precision]
+        c.kv_heads, c.head_dim = cfg.kv_heads, cfg.head_dim
+        c.rope_theta, c.norm_eps = cfg.rope_theta, cfg.norm_eps
         h = C.c_void_p()
         _lib.check(_lib.lib().lv_encoder_create(C.byref(c), C.cast(arr, C.POINTER(C.c_void_p)),
                                                 len(ws), device, C.byref(h)))

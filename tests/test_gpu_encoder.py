@@ -169,3 +169,62 @@ def test_attention_bf16_matches_torch(lv, n, S, H, dh, mode):
         q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2)).transpose(1, 2).reshape(n * S, -1)
     err = (out.float() - ref).abs().max().item()
     assert err < 3e-2, err
+
+
+# --------------------------------------------------------------------------- config-4 encoder
+
+@pytest.mark.parametrize("n,S,Hq,Hkv,dh,causal", [(2, 128, 4, 2, 64, True), (3, 256, 8, 8, 64, False),
+                                                 (2, 512, 16, 8, 128, True), (1, 192, 4, 1, 128, True)])
+def test_gqa_attention_matches_torch(lv, n, S, Hq, Hkv, dh, causal):
+    torch = _torch()
+    from paper_2506_08276_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(n * 7 + S + dh)
+    W = (Hq + 2 * Hkv) * dh
+    qkv = torch.randn(n * S, W, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty(n * S, Hq * dh, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().lv_attention_gqa_bf16(qkv.data_ptr(), out.data_ptr(), n, S, Hq, Hkv, dh,
+                                                int(causal), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    x = qkv.float().view(n, S, W)
+    q = x[..., :Hq * dh].view(n, S, Hq, dh).transpose(1, 2)
+    k = x[..., Hq * dh:(Hq + Hkv) * dh].view(n, S, Hkv, dh).repeat_interleave(Hq // Hkv, 2).transpose(1, 2)
+    v = x[..., (Hq + Hkv) * dh:].view(n, S, Hkv, dh).repeat_interleave(Hq // Hkv, 2).transpose(1, 2)
+    ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=causal)
+    ref = ref.transpose(1, 2).reshape(n * S, -1)
+    err = (out.float() - ref).abs().max().item()
+    assert err < 3e-2, err
+
+
+def _dec_cfg(name):
+    from paper_2506_08276_b200.encoder import ENCODERS, EncoderConfig
+    if name == "dh64":
+        return EncoderConfig("dec-dh64", 2, 256, 4, 512, 4000, 256, arch=1, kv_heads=2, head_dim=64)
+    if name == "dh128":
+        return EncoderConfig("dec-dh128", 2, 512, 4, 1024, 70000, 256, arch=1, kv_heads=2,
+                             head_dim=128)
+    q = ENCODERS["qwen3-0.6b"]  # the config-4 widths, 2 layers, a 20k vocabulary slice
+    return EncoderConfig("qwen3-2l", 2, q.hidden, q.heads, q.ffn, 20000, 512, arch=1,
+                         kv_heads=q.kv_heads, head_dim=q.head_dim)
+
+
+@pytest.mark.parametrize("name,S", [("dh64", 128), ("dh128", 256), ("qwen3", 512)])
+def test_decoder_encoder_close_to_torch(lv, name, S):
+    from oracle.encoder_ref import make_ref_encoder
+    from paper_2506_08276_b200.encoder import GpuEncoder, init_weights, synthetic_tokens
+    cfg = _dec_cfg(name)
+    w = init_weights(cfg, seed=31)
+    tok = synthetic_tokens(4, S, cfg.vocab, seed=32)
+    got = GpuEncoder(cfg, w, precision="bf16").encode(tok)
+    ref = make_ref_encoder(cfg, w).encode(tok.astype(np.int64))
+    cos = (got * ref).sum(1) / np.linalg.norm(got, axis=1) / np.linalg.norm(ref, axis=1)
+    assert cos.min() > 0.99, cos
+
+
+def test_decoder_encoder_batch_invariant(lv):
+    from paper_2506_08276_b200.encoder import GpuEncoder, init_weights, synthetic_tokens
+    cfg = _dec_cfg("dh64")
+    enc = GpuEncoder(cfg, init_weights(cfg, seed=4), precision="bf16")
+    tok = synthetic_tokens(11, 128, cfg.vocab, seed=5)
+    whole = enc.encode(tok)
+    parts = np.concatenate([enc.encode(tok[:3]), enc.encode(tok[3:])])
+    assert np.array_equal(whole, parts)

@@ -41,10 +41,12 @@ for name, a in sorted(agg.items(), key=lambda x: -x[1]["gpu__time_duration.sum"]
 
 if jout:
     ker = {}
-    for name, a in agg.items():
+    for name, a in agg.items():  # template instantiations aggregate under the base name
         short = name.split("::")[-1].split("<")[0].strip()
-        n = len(launches[name])
-        b = a.get("dram__bytes_read.sum", 0.0) + a.get("dram__bytes_write.sum", 0.0)
-        ker[short] = {"launches": n, "avg_us": a["gpu__time_duration.sum"] / n,
-                      "dram_bytes_per_launch": b / n}
+        k = ker.setdefault(short, {"launches": 0, "us": 0.0, "bytes": 0.0})
+        k["launches"] += len(launches[name])
+        k["us"] += a["gpu__time_duration.sum"]
+        k["bytes"] += a.get("dram__bytes_read.sum", 0.0) + a.get("dram__bytes_write.sum", 0.0)
+    ker = {s: {"launches": k["launches"], "avg_us": k["us"] / k["launches"],
+               "dram_bytes_per_launch": k["bytes"] / k["launches"]} for s, k in ker.items()}
     json.dump({"source": args[0], "kernels": ker}, open(jout, "w"), indent=1)
