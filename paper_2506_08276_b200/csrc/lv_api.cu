@@ -6,6 +6,8 @@
 // queries: matrix source = one persistent frontier launch; encoder source =
 // a host loop alternating frontier launches with one packed encoder forward
 // over every in-flight query's recompute request (dynamic batching).
+#include <cstdlib>
+#include <cstdio>
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -344,6 +346,15 @@ int lv_last_search_stats(const lv_index *ix, lv_search_stats *stats) {
 
 namespace {
 
+// LV_TRACE_ITERS=1: one stderr line per recompute iteration (profiling aid)
+bool trace_iters() {
+  static const bool on = [] {
+    const char *v = std::getenv("LV_TRACE_ITERS");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 // One pass of the batched search over B device-resident queries.
 int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const lv_search_params &p,
                 int aq_cap_override, int64_t *d_ids, float *d_dist, int32_t *d_count,
@@ -528,6 +539,9 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
         cudaEventElapsedTime(&ms, e0, e1);
         encoder_ms += ms;
         physical += n_new;
+        if (trace_iters())
+          std::fprintf(stderr, "[lv] iter %lld requests %d encoded %d encoder_ms %.3f\n",
+                       (long long)iterations, total, n_new, ms);
       } else if (ws.h_counters[2] >= B) {
         break;
       }
