@@ -214,7 +214,9 @@ int lv_attention_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int
 int lv_attention_gqa_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int32_t Hq,
                           int32_t Hkv, int32_t dh, int32_t causal, void *stream);
 /* GEMM kernel selection: 0 = auto (2-CTA cta_group::2 kernel when N % 256 == 0),
- * 1 = 1-CTA kernel only. Returns the previous mode. */
+ * 1 = 1-CTA kernel only; + 2 = 3-buffer/3-stage epilogue for short-K residual GEMMs
+ * (experiment; measured slower than the default 2-buffer/4-stage kernel).
+ * Returns the previous mode. */
 int lv_set_gemm_mode(int mode);
 /* Attention kernel selection: 0 = auto (tcgen05/TMEM kernel for dh == 64 and
  * S in {128, 256}, else the mma.sync kernel), 1 = mma.sync kernel only,

@@ -438,7 +438,8 @@ __global__ void __launch_bounds__(128) attn_flash_kernel(const __nv_bfloat16 *__
   __nv_bfloat16 *Qs = reinterpret_cast<__nv_bfloat16 *>(smem);
   __nv_bfloat16 *Ks = Qs + 64 * LD;       // [2][64][LD]
   __nv_bfloat16 *Vs = Ks + 2 * 64 * LD;   // [2][64][LD]
-  const int qb = blockIdx.x;
+  // causal: the longest rows (last q blocks) are scheduled first for a short tail
+  const int qb = CAUSAL ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
   const int seq = blockIdx.y / Hq, h = blockIdx.y % Hq, g = h / (Hq / Hkv);
   const int RS = (Hq + 2 * Hkv) * DH;
   const size_t row0 = (size_t)seq * S;

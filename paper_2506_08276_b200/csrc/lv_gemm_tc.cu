@@ -27,6 +27,7 @@
 #include "lv_tc.cuh"
 
 namespace lv {
+int g_short_k = 0;  // residual GEMMs with K <= this use the 3-buffer epilogue (off: measured slower)
 namespace {
 
 constexpr int kBM = 128;
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Shared-memory budget per CTA (<= 227 KB): residual GEMMs double-buffer the
 // epilogue boxes (residual prefetch one box ahead) and keep 4 operand stages;
 // the others single-buffer the output box and keep 5.
-template <bool kRes>
+template <int kMode>
 struct PairCfg;
 constexpr int kHalfBytes = 128 * kBK * 2;          // 16 KB: A or B half per stage
 constexpr int kStageBytes2 = 2 * kHalfBytes;        // per CTA
@@ -260,12 +261,17 @@ constexpr int kBoxBytes = 32 * 64 * 2;
 // per epilogue warp, two boxes' column vectors (bias, colc, gamma, beta: 64 fp32 each)
 constexpr int kColVecBytes = 4 * 64 * 4;
 constexpr int kColVecTotal = kEpiWarps * 2 * kColVecBytes;
-template <bool kRes>
+// kMode 0: no residual (1 box buffer, 5 stages); 1: residual, 2 box buffers,
+// 4 stages (long-K GEMMs); 2: residual, 3 box buffers, 3 stages (short-K
+// GEMMs, whose epilogue is the critical path: the residual load for box b+1
+// need not wait for the store of box b-1 to drain)
+template <int kMode>
 struct PairCfg {
-  static constexpr int kStages = kRes ? 4 : 5;
-  static constexpr int kBufs = kRes ? 2 : 1;  // epilogue boxes per warp
+  static constexpr bool kRes = kMode != 0;
+  static constexpr int kStages = kMode == 0 ? 5 : kMode == 1 ? 4 : 3;
+  static constexpr int kBufs = kMode == 0 ? 1 : kMode == 1 ? 2 : 3;  // epilogue boxes per warp
   static constexpr int kStagingBytes = kEpiWarps * kBufs * kBoxBytes;
-  static constexpr int kSmem = kStages * kStageBytes2 + kStagingBytes + kColVecTotal + 1024 + 256;
+  static constexpr int kSmem = kStages * kStageBytes2 + kStagingBytes + kColVecTotal + 1024 + 512;
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -413,7 +419,7 @@ __device__ __forceinline__ void epilogue_apply(const uint32_t (&r)[32], const Ep
   }
 }
 
-template <bool kRes>
+template <int kMode>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
@@ -425,8 +431,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
-  constexpr int kStages2 = PairCfg<kRes>::kStages;
-  constexpr int kStagingBytes = PairCfg<kRes>::kStagingBytes;
+  constexpr bool kRes = PairCfg<kMode>::kRes;
+  constexpr int kBufs = PairCfg<kMode>::kBufs;
+  constexpr int kStages2 = PairCfg<kMode>::kStages;
+  constexpr int kStagingBytes = PairCfg<kMode>::kStagingBytes;
   uint8_t *sB = smem + kStages2 * kHalfBytes;
   uint8_t *sStage = sB + kStages2 * kHalfBytes;
   float *sColVec = reinterpret_cast<float *>(sStage + kStagingBytes);
@@ -434,8 +442,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t *empty = full + kStages2;
   uint64_t *tfull = empty + kStages2;
   uint64_t *tempty = tfull + 2;
-  uint64_t *rbar = tempty + 2;  // [kEpiWarps][2] residual-box arrivals
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(rbar + 2 * kEpiWarps);
+  uint64_t *rbar = tempty + 2;  // [kEpiWarps][3] residual-box arrivals
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(rbar + 3 * kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -450,7 +458,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * kEpiWarps);
     }
-    for (int a = 0; a < 2 * kEpiWarps; ++a) mbar_init(&rbar[a], 1);
+    for (int a = 0; a < 3 * kEpiWarps; ++a) mbar_init(&rbar[a], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -538,8 +546,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int half = ew >> 2;
     const int fl = ep.flags;
     constexpr bool has_res = kRes;
-    uint8_t *stg = sStage + ew * PairCfg<kRes>::kBufs * kBoxBytes;
-    uint64_t *rb = rbar + 2 * ew;
+    uint8_t *stg = sStage + ew * kBufs * kBoxBytes;
+    uint64_t *rb = rbar + 3 * ew;
     uint32_t rph = 0;  // parity bit per buffer
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
     const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
@@ -593,8 +601,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       fence_after();
 #pragma unroll 1
       for (int b = 0; b < 2; ++b, ++blk) {
-        const int buf = blk & 1;  // column-vector buffer (and box buffer if double-buffered)
-        uint8_t *box = stg + (kRes ? buf * kBoxBytes : 0);
+        const int buf = blk & 1;            // column-vector buffer
+        const int bb = blk % kBufs;         // epilogue box buffer
+        const int nb = (blk + 1) % kBufs;   // the next box's buffer
+        uint8_t *box = stg + bb * kBoxBytes;
         int x, y;
         box_coords(tile, b, x, y);
         const int grow = y + lane;  // this thread's output row
@@ -641,11 +651,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (has_res) {
             const int nt = b == 0 ? tile : tile + n_pairs;
             if (nt < num_tiles) {
-              bulk_wait_read<0>();
+              bulk_wait_read<kBufs - 2>();  // the store that last used buffer nb has read it
               int nx, ny;
               box_coords(nt, b ^ 1, nx, ny);
-              mbar_expect_tx(&rb[buf ^ 1], kBoxBytes);
-              tma_load_2d(stg + (buf ^ 1) * kBoxBytes, &tmR, &rb[buf ^ 1], nx, ny, pol_r);
+              mbar_expect_tx(&rb[nb], kBoxBytes);
+              tma_load_2d(stg + nb * kBoxBytes, &tmR, &rb[nb], nx, ny, pol_r);
             }
           } else {
             bulk_wait_read<0>();  // the previous box's store has read the (single) buffer
@@ -653,8 +663,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         if (has_res) {
-          mbar_wait(&rb[buf], (rph >> buf) & 1);
-          rph ^= 1u << buf;
+          mbar_wait(&rb[bb], (rph >> bb) & 1);
+          rph ^= 1u << bb;
         }
         asm volatile("cp.async.wait_group 1;" ::: "memory");  // this box's column vectors
         __syncwarp();
@@ -798,22 +808,29 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
              LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(residual) failed");
   static bool attr_set = false;
   if (!attr_set) {
-    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<false>,
+    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       PairCfg<false>::kSmem));
-    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<true>,
+                                       PairCfg<0>::kSmem));
+    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       PairCfg<true>::kSmem));
+                                       PairCfg<1>::kSmem));
+    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PairCfg<2>::kSmem));
     attr_set = true;
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = std::min(tiles, tc_gemm_num_sms() / 2);
-  if (ep.flags & EPF_RES)
-    tc_gemm_pair_kernel<true><<<2 * pairs, kThreads, PairCfg<true>::kSmem, s>>>(ta, tb, to, tr, M,
-                                                                              N, K, ep);
+  const int mode = !(ep.flags & EPF_RES) ? 0 : (K <= g_short_k ? 2 : 1);
+  if (mode == 2)
+    tc_gemm_pair_kernel<2><<<2 * pairs, kThreads, PairCfg<2>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
+                                                                          ep);
+  else if (mode == 1)
+    tc_gemm_pair_kernel<1><<<2 * pairs, kThreads, PairCfg<1>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
+                                                                          ep);
   else
-    tc_gemm_pair_kernel<false><<<2 * pairs, kThreads, PairCfg<false>::kSmem, s>>>(ta, tb, to, tr,
-                                                                                M, N, K, ep);
+    tc_gemm_pair_kernel<0><<<2 * pairs, kThreads, PairCfg<0>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
+                                                                          ep);
   note_launch();
   LV_CHECK_CUDA(cudaGetLastError());
   return LV_OK;
