@@ -196,13 +196,15 @@ def recall_of(ids: np.ndarray, gt: np.ndarray) -> float:
     return hit / len(gt)
 
 
-def tune(W, cfg, args, dev_index):
+def tune(W, cfg, args, dev_index, hub_cache=None):
     """Per rerank percent, the minimal ef reaching the recall target (tune_ef,
-    evaluation.py:132-161, upper bound --ef-max instead of n); then the
-    (ef, rerank percent) pair with the fewest recomputations per query (the
-    encoder dominates the step). Evaluated in resident-matrix mode, which
-    returns the same results and counters as the recompute mode (the encoder
-    is batch-invariant)."""
+    evaluation.py:132-161, upper bound --ef-max instead of n), evaluated in
+    resident-matrix mode (same results as the recompute mode: the encoder is
+    batch-invariant). Then, for every feasible (ef, rerank percent), the
+    PHYSICAL encoder passages of one full step — the step's cost — are
+    measured with a dry recompute search (LV_DRY_RECOMPUTE: the same
+    shared-recompute table and hub cache, rows from the resident matrix), and
+    the pair with the fewest is chosen."""
     import paper_2506_08276_b200 as lv
     k = cfg["k"]
     Q = W["Q"][:cfg["n_queries"]].contiguous()   # tune on the config's query set
@@ -236,7 +238,17 @@ def tune(W, cfg, args, dev_index):
         table.append(dict(alpha=alpha, ef=lo, recall=memo[lo][0], recomputes=memo[lo][1],
                           feasible=True))
     ok = [t for t in table if t["feasible"]] or table
-    best = min(ok, key=lambda t: (t["recomputes"], -t["recall"]))
+    if W.get("prov") is not None:
+        batch = min(args.batch or cfg["batch"], W["Q"].shape[0])
+        for t in ok:
+            p = lv.SearchParams(k=k, ef=t["ef"], rerank_percent=t["alpha"])
+            dev_index.search_device(W["Q"][:batch].contiguous(), p, lv.ProviderSource(W["prov"]),
+                                    cache=hub_cache, dry_matrix=W["E"])
+            t["physical_per_query"] = dev_index.last_stats()["physical_encodes"] / batch
+            log(f"tune: alpha={t['alpha']} ef={t['ef']} physical/q={t['physical_per_query']:.1f}")
+        best = min(ok, key=lambda t: (t["physical_per_query"], -t["recall"]))
+    else:
+        best = min(ok, key=lambda t: (t["recomputes"], -t["recall"]))
     return best, table
 
 
@@ -312,7 +324,8 @@ def main():
                     help="rerank percents tried by the tuner (the first is used with --ef)")
     ap.add_argument("--corpus", default="", choices=["", "lda", "uniform"])
     ap.add_argument("--inflight", type=int, default=0, help="concurrent query slots per rank")
-    ap.add_argument("--n", type=int, default=0, help="override the corpus size (profiling only)")
+    ap.add_argument("--corpus-size", "--n", dest="n", type=int, default=0,
+                    help="override the corpus size (profiling only)")
     ap.add_argument("--cache-percent", type=float, default=2.0,
                     help="reference EmbeddingCache size (SearchParams.cache_percent)")
     ap.add_argument("--recall", type=float, default=0.90)
@@ -339,11 +352,19 @@ def main():
         log(f"note: WORLD_SIZE={world} but --gpus={args.gpus}")
     if args.impl == "reference" and rank != 0:
         return  # the reference arm is a CPU baseline: rank 0 alone runs it
+    # LV_BENCH_DEVICE / LV_BENCH_BACKEND: exercise the multi-rank path with
+    # several ranks on one GPU (gloo, since NCCL needs one GPU per rank) —
+    # testing only; the default is one rank per GPU over NCCL
+    local = int(os.environ.get("LV_BENCH_DEVICE", local))
+    backend = os.environ.get("LV_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dist = None
     if world > 1 and args.impl == "ours":
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import __graft_entry__ as ge
     ge.build()
     import paper_2506_08276_b200 as lv
@@ -353,12 +374,20 @@ def main():
 
     W = setup(cfg, args, local)
     dev_index = lv.search.device_index_for(W["graph"], W["model"], W["codes"])
+    prov = EncoderProvider(W["enc"], W["tok_dev"])
+    W["prov"] = prov
+    dev_index.attach_encoder(prov)  # the hub cache's rows are encoded when it is set
+    hub_cache = None
+    if args.cache_percent:
+        # reference EmbeddingCache (search.py:113-142): top-degree nodes' exact
+        # vectors pinned once (untimed setup), results-transparent
+        hub_cache = lv.build_embedding_cache(W["graph"], args.cache_percent)
     if args.ef:
         best = dict(alpha=args.alphas[0], ef=args.ef, recall=None, recomputes=None,
                     feasible=True)
         table = []
     else:
-        best, table = tune(W, cfg, args, dev_index)
+        best, table = tune(W, cfg, args, dev_index, hub_cache)
     ef, tuned_recall, feasible = best["ef"], best["recall"], best["feasible"]
     args.alpha = best["alpha"]
     log(f"chosen ef={ef} rerank={args.alpha}% (tuned recall {tuned_recall}, feasible={feasible})")
@@ -371,14 +400,9 @@ def main():
         run_reference(W, cfg, args, ef, batch, dev_index, params, flops_pp)
         return
 
-    prov = EncoderProvider(W["enc"], W["tok_dev"])
     source = lv.ProviderSource(prov)
-    hub_cache = None
-    if args.cache_percent:
-        # reference EmbeddingCache (search.py:113-142): top-degree nodes' exact
-        # vectors pinned once (untimed setup), results-transparent
-        hub_cache = lv.build_embedding_cache(W["graph"], args.cache_percent)
-        dev_index.attach_encoder(prov)
+    dev_index.attach_encoder(prov)
+    if hub_cache is not None:
         dev_index.set_cache(hub_cache)
     nq = W["Q"].shape[0]
 

@@ -69,6 +69,11 @@ extern "C" {
 #define LV_NO_SHARED_RECOMPUTE 2  /* lv_search_params.flags: encode every request, even
                                      when another in-flight query recomputed the node
                                      earlier in the same call (results are identical) */
+#define LV_DRY_RECOMPUTE 4   /* lv_search_params.flags, encoder source: fill recomputed rows
+                                from the resident matrix (lv_index_set_matrix) instead of
+                                running the encoder. Same results and counters (the encoder
+                                is batch-invariant); measures a configuration's physical
+                                recompute count cheaply (tuning) */
 
 /* per-query status codes written to lv_search_outputs.status */
 #define LV_Q_OK 0

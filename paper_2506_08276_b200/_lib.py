@@ -19,6 +19,7 @@ LV_SOURCE_MATRIX = 0
 LV_SOURCE_ENCODER = 1
 LV_IO_DEVICE = 1
 LV_NO_SHARED_RECOMPUTE = 2
+LV_DRY_RECOMPUTE = 4
 
 
 class IndexDesc(C.Structure):

@@ -355,6 +355,9 @@ bool trace_iters() {
   return on;
 }
 
+__global__ void gather_rows_kernel(const float *src, const int32_t *idx, int64_t n, int dim,
+                                   float *dst);
+
 // One pass of the batched search over B device-resident queries.
 int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const lv_search_params &p,
                 int aq_cap_override, int64_t *d_ids, float *d_dist, int32_t *d_count,
@@ -489,8 +492,10 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
     cudaEventElapsedTime(&frontier_ms, e0, e1);
     iterations = 1;
   } else {
-    LV_REQUIRE(ix->enc && ix->tokens, LV_ERR_USAGE,
-               "encoder source requires lv_index_attach_encoder");
+    const bool dry = (p.flags & LV_DRY_RECOMPUTE) != 0;
+    LV_REQUIRE(dry ? ix->matrix != nullptr : (ix->enc && ix->tokens), LV_ERR_USAGE,
+               dry ? "LV_DRY_RECOMPUTE requires lv_index_set_matrix"
+                   : "encoder source requires lv_index_attach_encoder");
     int32_t row_base = 0;
     auto reset_table = [&]() -> int {
       LV_CHECK_CUDA(cudaMemsetAsync(ws.hkeys.ptr, 0xff, ((size_t)hmask + 1) * 4, s));
@@ -531,9 +536,15 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
           row_base = ws.h_counters[3];
         }
         cudaEventRecord(e0, s);
-        if (n_new > 0)
+        if (n_new > 0 && dry) {
+          gather_rows_kernel<<<(unsigned)(((int64_t)n_new * ix->dim + 255) / 256), 256, 0, s>>>(
+              ix->matrix, enc_ids, n_new, ix->dim, enc_out);
+          note_launch();
+          LV_CHECK_CUDA(cudaGetLastError());
+        } else if (n_new > 0) {
           LV_TRY(encode_node_rows(ix->enc, ix->tokens, ix->token_bytes, ix->seq_len, enc_ids,
                                   n_new, enc_out, s));
+        }
         cudaEventRecord(e1, s);
         LV_CHECK_CUDA(cudaEventSynchronize(e1));
         cudaEventElapsedTime(&ms, e0, e1);

@@ -27,6 +27,9 @@ def gather_results(ids, dist_, group=None):
         return ids, dist_
     ids = ids.contiguous()
     dist_ = dist_.contiguous()
+    if ids.is_cuda and dist.get_backend(group) != "nccl":  # gloo: gather through the host
+        gi, gd = gather_results(ids.cpu(), dist_.cpu(), group)
+        return gi.to(ids.device), gd.to(dist_.device)
     if ids.is_cuda:
         g_ids = torch.empty((world * ids.shape[0],) + tuple(ids.shape[1:]), dtype=ids.dtype,
                             device=ids.device)
@@ -48,6 +51,8 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     import torch.distributed as dist
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return float(value)
+    if dist.get_backend(group) != "nccl":
+        device = None
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
@@ -58,6 +63,8 @@ def sum_over_ranks(values, device=None, group=None) -> list:
     import torch.distributed as dist
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return [float(v) for v in values]
+    if dist.get_backend(group) != "nccl":
+        device = None
     t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
     dist.all_reduce(t, group=group)
     return [float(v) for v in t.tolist()]

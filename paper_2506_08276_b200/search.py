@@ -295,6 +295,10 @@ class DeviceIndex:
         if isinstance(source, MatrixSource):
             p.source = _lib.LV_SOURCE_MATRIX
             self.set_matrix(source.matrix)
+        elif isinstance(source, ProviderSource) and dry_matrix is not None:
+            p.source = _lib.LV_SOURCE_ENCODER
+            p.flags |= _lib.LV_DRY_RECOMPUTE
+            self.set_matrix(dry_matrix)
         elif isinstance(source, ProviderSource):
             p.source = _lib.LV_SOURCE_ENCODER
             self.attach_encoder(source.provider)
@@ -353,12 +357,16 @@ class DeviceIndex:
 
     def search_device(self, Q, params: SearchParams, source, qn=None,
                       cache: EmbeddingCache | None = None, max_inflight: int = 0,
-                      out: dict | None = None, shared_recompute: bool = True):
+                      out: dict | None = None, shared_recompute: bool = True,
+                      dry_matrix=None):
         """Device-resident batch search: ``Q`` is a CUDA float32 tensor [B, dim],
         ``qn`` a CUDA tensor [B] or None (norms then computed on the device).
         Returns CUDA tensors ids [B, k] (int64, -1 padded), dist [B, k],
         count [B], counters [B, 4] (recomputations, approx_lookups, cache_hits,
-        expansions). Stream-ordered on the current torch stream."""
+        expansions). Stream-ordered on the current torch stream.
+        ``dry_matrix`` (with a ProviderSource): rows the encoder would produce,
+        used instead of running it (LV_DRY_RECOMPUTE) — same results, counters
+        and physical-recompute statistics, for tuning."""
         import torch
         if not (Q.is_cuda and Q.dtype == torch.float32 and Q.is_contiguous() and Q.dim() == 2):
             raise InvalidArgumentError("Q must be a contiguous CUDA float32 [B, dim] tensor")
@@ -375,6 +383,10 @@ class DeviceIndex:
         if isinstance(source, MatrixSource):
             p.source = _lib.LV_SOURCE_MATRIX
             self.set_matrix(source.matrix)
+        elif isinstance(source, ProviderSource) and dry_matrix is not None:
+            p.source = _lib.LV_SOURCE_ENCODER
+            p.flags |= _lib.LV_DRY_RECOMPUTE
+            self.set_matrix(dry_matrix)
         elif isinstance(source, ProviderSource):
             p.source = _lib.LV_SOURCE_ENCODER
             self.attach_encoder(source.provider)
