@@ -221,9 +221,14 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStageBytes);
+  // Q|K and V of a stage have separate full/empty barriers: Q and K are free
+  // once the item's last Q.K^T MMA completes, so the next item's Q|K load
+  // starts a softmax earlier than a per-stage release would allow
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStageBytes);  // Q|K
   uint64_t *empty = full + 2;
-  uint64_t *s_full = empty + 2;
+  uint64_t *full_v = empty + 2;
+  uint64_t *empty_v = full_v + 2;
+  uint64_t *s_full = empty_v + 2;
   uint64_t *p_full = s_full + 2;
   uint64_t *o_full = p_full + 2;
   uint64_t *r_free = o_full + 2;
@@ -234,6 +239,8 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
+      mbar_init(&full_v[i], 1);
+      mbar_init(&empty_v[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
       mbar_init(&o_full[i], 1);
@@ -268,10 +275,12 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
         const int item = (int)blockIdx.x + i * (int)gridDim.x;
         const int seq = item / H, h = item - seq * H;
         uint8_t *base = smem + st * C::kStageBytes;
-        mbar_expect_tx(&full[st], C::kStageBytes);
+        mbar_expect_tx(&full[st], 2 * C::kTileBytes);
         tma_load_2d(base, &tm, &full[st], h * 64, seq * S, pol);
         tma_load_2d(base + C::kTileBytes, &tm, &full[st], D + h * 64, seq * S, pol);
-        tma_load_2d(base + 2 * C::kTileBytes, &tm, &full[st], 2 * D + h * 64, seq * S, pol);
+        mbar_wait(&empty_v[st], ((i >> 1) & 1) ^ 1);
+        mbar_expect_tx(&full_v[st], C::kTileBytes);
+        tma_load_2d(base + 2 * C::kTileBytes, &tm, &full_v[st], 2 * D + h * 64, seq * S, pol);
       }
     }
   } else if (warp == 1) {
@@ -289,9 +298,11 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) umma_ss(tmem + r * 256, a + 2 * k, b + 2 * k, idesc_s, k);
         umma_commit(&s_full[r]);
+        if (t == C::kQTiles - 1) umma_commit(&empty[i & 1]);  // Q|K of the stage consumed
       };
       auto issue_pv = [&](int j) {
         const int i = j / C::kQTiles, t = j % C::kQTiles, r = j & 1;
+        if (t == 0) mbar_wait(&full_v[i & 1], (i >> 1) & 1);
         mbar_wait(&p_full[r], (j >> 1) & 1);
         fence_after();
         const uint8_t *base = smem + (i & 1) * C::kStageBytes;
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
           umma_ts(tmem + r * 256 + S / 2, tmem + r * 256 + 8 * k, v + (uint64_t)(128 * k), idesc_o,
                   k);
         umma_commit(&o_full[r]);
-        if (t == C::kQTiles - 1) umma_commit(&empty[i & 1]);
+        if (t == C::kQTiles - 1) umma_commit(&empty_v[i & 1]);
       };
       if (total > 0) issue_s(0);
       if (total > 1) issue_s(1);
