@@ -267,9 +267,10 @@ constexpr int kColVecTotal = kEpiWarps * 2 * kColVecBytes;
 // need not wait for the store of box b-1 to drain)
 template <int kMode>
 struct PairCfg {
-  static constexpr bool kRes = kMode != 0;
-  static constexpr int kStages = kMode == 0 ? 5 : kMode == 1 ? 4 : 3;
-  static constexpr int kBufs = kMode == 0 ? 1 : kMode == 1 ? 2 : 3;  // epilogue boxes per warp
+  // kMode 3: SwiGLU epilogue (no residual; gate/up interleaved per 64 columns)
+  static constexpr bool kRes = kMode == 1 || kMode == 2;
+  static constexpr int kStages = (kMode == 0 || kMode == 3) ? 5 : kMode == 1 ? 4 : 3;
+  static constexpr int kBufs = (kMode == 0 || kMode == 3) ? 1 : kMode == 1 ? 2 : 3;  // boxes per warp
   static constexpr int kStagingBytes = kEpiWarps * kBufs * kBoxBytes;
   static constexpr int kSmem = kStages * kStageBytes2 + kStagingBytes + kColVecTotal + 1024 + 512;
 };
@@ -534,6 +535,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
+  } else if constexpr (kMode == 3) {
+    // SwiGLU epilogue: the weight rows are interleaved per 64 (gate block g,
+    // then up block g), so a warp's 128 accumulator columns hold gate and up
+    // of the same 64 output columns: out = silu(gate) * up, one [32 x 64]
+    // output box per tile and warp (output width N / 2). Bias-free.
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    uint8_t *box = sStage + ew * kBoxBytes;
+    const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
+    const uint32_t tempty_leader1 = map_to_rank(&tempty[1], 0);
+    const uint32_t row_off = (uint32_t)lane * 128;
+    const uint32_t sw = (uint32_t)(lane & 7);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+      const int y = (tile / n_tiles) * 256 + (int)rank * 128 + q * 32;
+      const int xo = (tile % n_tiles) * (BN / 2) + half * 64;
+      mbar_wait(&tfull[acc], acc_phase);
+      fence_after();
+      if (lane == 0) bulk_wait_read<0>();  // the previous tile's store has read the box
+      __syncwarp();
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t g[32], u[32];
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) +
+                            (uint32_t)(acc * BN + half * 128 + c * 32);
+        tmem_ld32_nowait(ta, g);
+        tmem_ld32_nowait(ta + 64, u);
+        tmem_ld_wait();
+        if (c == 1) {  // accumulator fully read
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float g0 = __uint_as_float(g[8 * k + 2 * e]), g1 = __uint_as_float(g[8 * k + 2 * e + 1]);
+            const float s0 = __fdividef(g0, 1.f + __expf(-g0)), s1 = __fdividef(g1, 1.f + __expf(-g1));
+            w[e] = pack_bf16(s0 * __uint_as_float(u[8 * k + 2 * e]),
+                             s1 * __uint_as_float(u[8 * k + 2 * e + 1]));
+          }
+          *reinterpret_cast<uint4 *>(box + row_off + (((uint32_t)(c * 4 + k) ^ sw) << 4)) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(&tmO, box, xo, y);
+        bulk_commit();
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (lane == 0) bulk_wait<0>();
   } else {
     // Epilogue: each warp owns 32 accumulator rows (its TMEM lane quarter) x
     // 128 columns (its half), processed as two 64-column boxes. A box goes
@@ -802,7 +862,8 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
   CUtensorMap ta, tb, to, tr;
   LV_REQUIRE(make_map(&ta, A, M, K, 128), LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(A) failed");
   LV_REQUIRE(make_map(&tb, W, N, K, 128), LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(W) failed");
-  LV_REQUIRE(make_tma_2d_bf16(&to, out, N, M, (uint64_t)N * 2, 64, 32), LV_ERR_INTERNAL,
+  const int n_out = (ep.flags & EPF_SWIGLU) ? N / 2 : N;
+  LV_REQUIRE(make_tma_2d_bf16(&to, out, n_out, M, (uint64_t)n_out * 2, 64, 32), LV_ERR_INTERNAL,
              "cuTensorMapEncodeTiled(out) failed");
   LV_REQUIRE(make_tma_2d_bf16(&tr, residual ? residual : out, N, M, (uint64_t)N * 2, 64, 32),
              LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(residual) failed");
@@ -817,12 +878,18 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<2>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<2>::kSmem));
+    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<3>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PairCfg<3>::kSmem));
     attr_set = true;
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = std::min(tiles, tc_gemm_num_sms() / 2);
-  const int mode = !(ep.flags & EPF_RES) ? 0 : (K <= g_short_k ? 2 : 1);
-  if (mode == 2)
+  const int mode = (ep.flags & EPF_SWIGLU) ? 3 : !(ep.flags & EPF_RES) ? 0 : (K <= g_short_k ? 2 : 1);
+  if (mode == 3)
+    tc_gemm_pair_kernel<3><<<2 * pairs, kThreads, PairCfg<3>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
+                                                                          ep);
+  else if (mode == 2)
     tc_gemm_pair_kernel<2><<<2 * pairs, kThreads, PairCfg<2>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
                                                                           ep);
   else if (mode == 1)
@@ -869,7 +936,10 @@ int tc_gemm_ex(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloat
                __nv_bfloat16 *out, int M, int N, int K, const EpiParams &ep, cudaStream_t s) {
   LV_REQUIRE(M >= 1 && N % 256 == 0 && K % kBK == 0 && K > 0, LV_ERR_USAGE,
              "tc_gemm_ex: need N % 256 == 0 and K % 64 == 0");
-  LV_REQUIRE(ep.bias != nullptr, LV_ERR_USAGE, "tc_gemm_ex: bias required");
+  LV_REQUIRE(ep.bias != nullptr || (ep.flags & EPF_SWIGLU), LV_ERR_USAGE,
+             "tc_gemm_ex: bias required");
+  LV_REQUIRE(!(ep.flags & EPF_SWIGLU) || ep.flags == EPF_SWIGLU, LV_ERR_USAGE,
+             "tc_gemm_ex: the SwiGLU epilogue combines with no other flag");
   LV_REQUIRE(!(ep.flags & EPF_RES) || residual != nullptr, LV_ERR_USAGE,
              "tc_gemm_ex: residual required");
   LV_REQUIRE(!(ep.flags & EPF_LN_IN) || (ep.colc && ep.ln_in), LV_ERR_USAGE,

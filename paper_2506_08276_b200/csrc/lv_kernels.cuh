@@ -33,7 +33,11 @@ struct TcGemmPlan;  // cached tensor maps for one (A, W, M, N, K)
 //   v += (res - mean_r) * rstd_r * res_g + res_b     (EPF_RES | EPF_RES_LN)
 //   stats[row][col / 64] = (mean, M2) of the bf16-rounded outputs of each
 //        64-column box (EPF_STATS; combined by ln_stats_finalize)
-enum EpiFlag : int { EPF_GELU = 1, EPF_RES = 2, EPF_RES_LN = 4, EPF_LN_IN = 8, EPF_STATS = 16 };
+//   out[:, j] = silu(acc[:, g(j)]) * acc[:, u(j)]   (EPF_SWIGLU, alone: weight
+//        rows interleaved per 64 as [gate 64 | up 64]; output width N / 2)
+enum EpiFlag : int {
+  EPF_GELU = 1, EPF_RES = 2, EPF_RES_LN = 4, EPF_LN_IN = 8, EPF_STATS = 16, EPF_SWIGLU = 32
+};
 struct EpiParams {
   const float *bias = nullptr;    // [N]
   const float *colc = nullptr;    // [N]  EPF_LN_IN
