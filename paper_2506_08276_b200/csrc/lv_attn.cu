@@ -676,6 +676,332 @@ cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// attn_tc_causal_kernel: causal grouped-query attention on the 5th-gen tensor
+// cores for the decoder-style encoder (config-4: dh = 128, S % 128 == 0).
+//
+// Work item = one 128-row query tile t of one (sequence, q head); its keys are
+// the (t + 1) 128-key blocks up to the diagonal. Two passes over the key
+// blocks replace the online rescaling of O (which would need O read-modify-
+// written in TMEM between P.V MMAs): pass A computes S = Q.K_b^T per block for
+// the exact row max; pass B recomputes S, writes P = 2^(s*c - max*c) (bf16,
+// masked above the diagonal) over the scores in TMEM and accumulates
+// O += P.V_b (TS-MMA, V as an MN-major operand spanning two 64-column swizzle
+// atoms). Q.K^T runs twice (1.5x the attention MMA work), cheap next to the
+// softmax exponentials.
+//   warp 0 / 10  TMA producers of softmax group 0 / 1 (Q, then the K blocks of
+//                pass A, then K, V of pass B through a 2-slot ring per group)
+//   warp 1       single MMA issuer; polls both groups' barriers and issues
+//                whichever operation is ready
+//   warps 2-9    two softmax groups of 4 warps (one TMEM lane quarter each);
+//                group r owns TMEM columns [256 r, 256 r + 256): S/P in the
+//                first 128, O in the second, and every second work item
+namespace atq {
+constexpr int kThreads = 11 * 32;
+constexpr int kTile = 128 * 128 * 2;        // [128][128] bf16 = two 64-column atoms
+constexpr int kGroupBytes = 3 * kTile;      // Q + 2 ring slots
+constexpr int kSmem = 2 * kGroupBytes + 1024 + 512;
+}  // namespace atq
+
+__global__ void __launch_bounds__(atq::kThreads, 1)
+    attn_tc_causal_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out,
+                          int n_seqs, int S, int Hq, int Hkv) {
+  using namespace tc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 2 * atq::kGroupBytes);
+  // per group r: [0] q_full [1] q_free [2,3] ring_full [4,5] ring_free [6] s_full
+  // [7] s_free [8] p_full [9] pv_done [10] o_full [11] o_free
+  auto B = [&](int r, int i) { return bars + r * 12 + i; };
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 24);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < 2; ++r) {
+      mbar_init(B(r, 0), 1);
+      mbar_init(B(r, 1), 1);
+      for (int k = 2; k < 6; ++k) mbar_init(B(r, k), 1);
+      mbar_init(B(r, 6), 1);
+      mbar_init(B(r, 7), 4);
+      mbar_init(B(r, 8), 4);
+      mbar_init(B(r, 9), 1);
+      mbar_init(B(r, 10), 1);
+      mbar_init(B(r, 11), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const int nT = S / 128;
+  const int n_items = n_seqs * Hq * nT;
+  const int RS = (Hq + 2 * Hkv) * 128;  // qkv row width
+  // local items of this CTA: j = 0, 1, ...; item = blockIdx.x + j * gridDim.x,
+  // t-major decode (longest tiles first), group r = j & 1
+  const int n_local =
+      n_items > (int)blockIdx.x ? (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
+                                : 0;
+  auto decode = [&](int j, int &seq, int &h, int &t) {
+    const int item = (int)blockIdx.x + j * (int)gridDim.x;
+    const int per_t = n_seqs * Hq;
+    t = nT - 1 - item / per_t;
+    const int rem = item % per_t;
+    seq = rem / Hq;
+    h = rem % Hq;
+  };
+
+  if (warp == 0 || warp == 10) {
+    const int r = warp == 0 ? 0 : 1;
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tm) : "memory");
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      uint8_t *qs = smem + r * atq::kGroupBytes;
+      uint8_t *ring = qs + atq::kTile;
+      uint32_t nq = 0, nr = 0;  // Q loads / ring loads so far
+      auto load_tile = [&](uint8_t *dst, uint64_t *bar, int col, int row) {
+        mbar_expect_tx(bar, atq::kTile);
+        tma_load_2d(dst, &tm, bar, col, row, pol);
+        tma_load_2d(dst + atq::kTile / 2, &tm, bar, col + 64, row, pol);
+      };
+      auto ring_load = [&](int col, int row) {
+        const int sl = nr & 1;
+        mbar_wait(B(r, 4 + sl), ((nr >> 1) & 1) ^ 1);
+        load_tile(ring + sl * atq::kTile, B(r, 2 + sl), col, row);
+        ++nr;
+      };
+      for (int j = r; j < n_local; j += 2) {
+        int seq, h, t;
+        decode(j, seq, h, t);
+        const int g = h / (Hq / Hkv);
+        const int row0 = seq * S;
+        mbar_wait(B(r, 1), (nq & 1) ^ 1);
+        load_tile(qs, B(r, 0), h * 128, row0 + t * 128);
+        ++nq;
+        for (int kb = 0; kb <= t; ++kb) ring_load((Hq + g) * 128, row0 + kb * 128);
+        for (int kb = 0; kb <= t; ++kb) {
+          ring_load((Hq + g) * 128, row0 + kb * 128);
+          ring_load((Hq + Hkv + g) * 128, row0 + kb * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16(128, 128);
+      constexpr uint32_t idesc_o = idesc_bf16(128, 128, true);
+      struct GS {
+        int j, t, op;          // local item, its tile, next op index within the item
+        uint32_t nq, nr;       // Q loads consumed / ring slots consumed
+        uint32_t ns, npv;      // S ops issued / P.V ops issued (this group)
+        uint32_t nsa;          // pass-A S ops whose s_free is awaited
+        bool prev_pv;          // the previous S op was followed by a P.V reading P
+        uint32_t nitems;       // items started (o_free parity)
+      } gs[2];
+      for (int r = 0; r < 2; ++r) {
+        gs[r] = GS{r, 0, 0, 0, 0, 0, 0, 0, false, 0};
+        if (r < n_local) {
+          int a, b2;
+          decode(r, a, b2, gs[r].t);
+        }
+      }
+      int done = 0;
+      const int want = (n_local > 0) + (n_local > 1);
+      while (done < want) {
+        for (int r = 0; r < 2; ++r) {
+          GS &G = gs[r];
+          if (G.j >= n_local) continue;
+          const int t = G.t;
+          const int nA = t + 1;
+          const int nops = nA + 2 * (t + 1);
+          const int op = G.op;
+          const uint32_t rb = tmem + r * 256;
+          const uint8_t *qs = smem + r * atq::kGroupBytes;
+          const uint8_t *ring = qs + atq::kTile;
+          const bool is_s = op < nA || ((op - nA) & 1) == 0;
+          const int sl = G.nr & 1;
+          if (!mbar_test(B(r, 2 + sl), (G.nr >> 1) & 1)) continue;  // operand tile landed
+          if (is_s) {
+            if (op == 0 && !mbar_test(B(r, 0), G.nq & 1)) continue;  // Q landed
+            // the S/P region is free: the softmax consumed the previous pass-A
+            // S, or the P.V that read the previous P completed
+            if (G.ns > 0) {
+              if (G.prev_pv) {
+                if (!mbar_test(B(r, 9), (G.npv - 1) & 1)) continue;
+              } else if (!mbar_test(B(r, 7), (G.nsa - 1) & 1)) {
+                continue;
+              }
+            }
+            fence_after();
+            const uint64_t a = sw128_desc(smem_u32(qs));
+            const uint64_t b = sw128_desc(smem_u32(ring + sl * atq::kTile));
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {  // K = 128: two 64-column atoms, 4 steps each
+              const uint64_t off = (uint64_t)((k >> 2) * (atq::kTile / 2 / 16) + 2 * (k & 3));
+              umma_ss(rb, a + off, b + off, idesc_s, k);
+            }
+            umma_commit(B(r, 6));
+            umma_commit(B(r, 4 + sl));
+            ++G.ns;
+            if (op < nA) {
+              ++G.nsa;
+              G.prev_pv = false;
+            } else {
+              G.prev_pv = true;
+            }
+            if (op == nops - 2) umma_commit(B(r, 1));  // last Q.K^T: Q slot free
+          } else {
+            const int kb = (op - nA) >> 1;
+            if (!mbar_test(B(r, 8), G.npv & 1)) continue;                       // P written
+            if (kb == 0 && !mbar_test(B(r, 11), (G.nitems & 1) ^ 1)) continue;  // O drained
+            fence_after();
+            const uint64_t v = sw128_desc(smem_u32(ring + sl * atq::kTile), 1024, atq::kTile / 2);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)  // 16 keys per step = 2048 B of each V atom
+              umma_ts(rb + 128, rb + 8 * k, v + (uint64_t)(128 * k), idesc_o, kb > 0 || k > 0);
+            umma_commit(B(r, 9));
+            umma_commit(B(r, 4 + sl));
+            ++G.npv;
+            if (kb == t) umma_commit(B(r, 10));
+          }
+          ++G.nr;
+          if (op == 0) ++G.nq;
+          G.op = op + 1;
+          if (G.op == nops) {  // next item of this group
+            G.op = 0;
+            ++G.nitems;
+            G.j += 2;
+            if (G.j < n_local) {
+              int a, b2;
+              decode(G.j, a, b2, G.t);
+            } else {
+              ++done;
+            }
+          }
+        }
+      }
+    }
+  } else {
+    const int g = (warp - 2) >> 2;
+    const int q = warp & 3;
+    const int rrow = q * 32 + lane;
+    const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * 256);
+    constexpr float kC = 0.12751743082459868f;  // log2(e) / sqrt(128)
+    uint32_t ns = 0, nitems = 0;
+    for (int j = g; j < n_local; j += 2, ++nitems) {
+      int seq, h, t;
+      decode(j, seq, h, t);
+      const int qi = t * 128 + rrow;  // query position
+      float m = -FLT_MAX;
+      for (int kb = 0; kb <= t; ++kb, ++ns) {  // pass A: row max
+        mbar_wait(B(g, 6), ns & 1);
+        fence_after();
+        uint32_t r0[32], r1[32];
+#pragma unroll
+        for (int c = 0; c < 128; c += 64) {
+          tmem_ld32_nowait(tb + c, r0);
+          tmem_ld32_nowait(tb + c + 32, r1);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int k0 = kb * 128 + c + e;
+            const float a0 = k0 <= qi ? __uint_as_float(r0[e]) : -FLT_MAX;
+            const float a1 = k0 + 32 <= qi ? __uint_as_float(r1[e]) : -FLT_MAX;
+            m = fmaxf(m, fmaxf(a0, a1));
+          }
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(B(g, 7));
+      }
+      const float mc = m * kC;
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int kb = 0; kb <= t; ++kb, ++ns) {  // pass B: P over the scores
+        mbar_wait(B(g, 6), ns & 1);
+        fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t r0[32];
+          tmem_ld32(tb + c, r0);
+          uint32_t w[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int k0 = kb * 128 + c + 2 * e;
+            const float p0 = k0 <= qi ? ex2_approx(fmaf(__uint_as_float(r0[2 * e]), kC, -mc)) : 0.f;
+            const float p1 =
+                k0 + 1 <= qi ? ex2_approx(fmaf(__uint_as_float(r0[2 * e + 1]), kC, -mc)) : 0.f;
+            s4[(2 * e) & 3] += p0;
+            s4[(2 * e + 1) & 3] += p1;
+            w[e] = pack_bf16(p0, p1);
+          }
+          tmem_st16(tb + c / 2, w);
+        }
+        tmem_st_wait();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(B(g, 8));
+      }
+      // epilogue: O / rowsum -> context row slice [h*128, +128)
+      mbar_wait(B(g, 10), nitems & 1);
+      fence_after();
+      uint32_t o[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32_nowait(tb + 128 + 32 * c, o[c]);
+      tmem_ld_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(B(g, 11));
+      const float inv = 1.f / ((s4[0] + s4[1]) + (s4[2] + s4[3]));
+      uint4 *op = reinterpret_cast<uint4 *>(out + ((size_t)seq * S + qi) * (size_t)(Hq * 128) +
+                                            h * 128);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 u;
+          u.x = pack_bf16(__uint_as_float(o[c][8 * v + 0]) * inv, __uint_as_float(o[c][8 * v + 1]) * inv);
+          u.y = pack_bf16(__uint_as_float(o[c][8 * v + 2]) * inv, __uint_as_float(o[c][8 * v + 3]) * inv);
+          u.z = pack_bf16(__uint_as_float(o[c][8 * v + 4]) * inv, __uint_as_float(o[c][8 * v + 5]) * inv);
+          u.w = pack_bf16(__uint_as_float(o[c][8 * v + 6]) * inv, __uint_as_float(o[c][8 * v + 7]) * inv);
+          op[4 * c + v] = u;
+        }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+cudaError_t launch_attn_tc_causal(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S,
+                                  int Hq, int Hkv, cudaStream_t s) {
+  CUtensorMap tm;
+  const uint64_t W = (uint64_t)(Hq + 2 * Hkv) * 128;
+  if (!make_tma_2d_bf16(&tm, qkv, W, (uint64_t)n_seqs * S, W * 2, 64, 128))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_causal_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, atq::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int items = n_seqs * Hq * (S / 128);
+  const int grid = std::min(items, tc_gemm_num_sms());
+  attn_tc_causal_kernel<<<grid, atq::kThreads, atq::kSmem, s>>>(tm, out, n_seqs, S, Hq, Hkv);
+  note_launch();
+  return cudaGetLastError();
+}
+
+
 cudaError_t attention_gqa_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S,
                                int Hq, int Hkv, int dh, bool causal, cudaStream_t s) {
   if (n_seqs <= 0) return cudaSuccess;
@@ -683,6 +1009,9 @@ cudaError_t attention_gqa_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int
   if (dh == 64)
     return causal ? launch_flash<64, true>(qkv, out, n_seqs, S, Hq, Hkv, s)
                   : launch_flash<64, false>(qkv, out, n_seqs, S, Hq, Hkv, s);
+  if (dh == 128 && causal && S % 128 == 0 && g_attn_mode != 1 &&
+      ((uintptr_t)qkv & 15) == 0 && ((uintptr_t)out & 15) == 0)
+    return launch_attn_tc_causal(qkv, out, n_seqs, S, Hq, Hkv, s);
   if (dh == 128)
     return causal ? launch_flash<128, true>(qkv, out, n_seqs, S, Hq, Hkv, s)
                   : launch_flash<128, false>(qkv, out, n_seqs, S, Hq, Hkv, s);

@@ -173,18 +173,28 @@ def test_attention_bf16_matches_torch(lv, n, S, H, dh, mode):
 
 # --------------------------------------------------------------------------- config-4 encoder
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("n,S,Hq,Hkv,dh,causal", [(2, 128, 4, 2, 64, True), (3, 256, 8, 8, 64, False),
-                                                 (2, 512, 16, 8, 128, True), (1, 192, 4, 1, 128, True)])
-def test_gqa_attention_matches_torch(lv, n, S, Hq, Hkv, dh, causal):
+                                                 (2, 512, 16, 8, 128, True), (1, 192, 4, 1, 128, True),
+                                                 (3, 256, 4, 2, 128, True), (40, 512, 16, 8, 128, True),
+                                                 (1, 128, 2, 2, 128, True)])
+def test_gqa_attention_matches_torch(lv, n, S, Hq, Hkv, dh, causal, mode):
+    """mode 0: tcgen05 causal kernel where it applies (dh 128, S % 128 == 0), else the
+    mma.sync flash kernel; mode 1: the flash kernel everywhere."""
     torch = _torch()
     from paper_2506_08276_b200 import _lib
+    prev = _lib.lib().lv_set_attention_mode(mode)
     g = torch.Generator(device="cuda").manual_seed(n * 7 + S + dh)
     W = (Hq + 2 * Hkv) * dh
     qkv = torch.randn(n * S, W, device="cuda", generator=g).to(torch.bfloat16)
     out = torch.empty(n * S, Hq * dh, device="cuda", dtype=torch.bfloat16)
-    _lib.check(_lib.lib().lv_attention_gqa_bf16(qkv.data_ptr(), out.data_ptr(), n, S, Hq, Hkv, dh,
-                                                int(causal), torch.cuda.current_stream().cuda_stream))
-    torch.cuda.synchronize()
+    try:
+        _lib.check(_lib.lib().lv_attention_gqa_bf16(qkv.data_ptr(), out.data_ptr(), n, S, Hq, Hkv,
+                                                    dh, int(causal),
+                                                    torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+    finally:
+        _lib.lib().lv_set_attention_mode(prev)
     x = qkv.float().view(n, S, W)
     q = x[..., :Hq * dh].view(n, S, Hq, dh).transpose(1, 2)
     k = x[..., Hq * dh:(Hq + Hkv) * dh].view(n, S, Hkv, dh).repeat_interleave(Hq // Hkv, 2).transpose(1, 2)
