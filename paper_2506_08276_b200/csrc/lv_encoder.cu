@@ -369,10 +369,13 @@ __global__ void rmsnorm_bf16_kernel(const __nv_bfloat16 *__restrict__ in,
     const int c0 = (i * 32 + lane) * 8;
     uint4 u;
     uint32_t *w = reinterpret_cast<uint32_t *>(&u);
+    const float4 g0 = __ldg(reinterpret_cast<const float4 *>(g + c0));
+    const float4 g1 = __ldg(reinterpret_cast<const float4 *>(g + c0 + 4));
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      __nv_bfloat162 hh = __floats2bfloat162_rn(v[i][2 * e] * r * __ldg(g + c0 + 2 * e),
-                                                v[i][2 * e + 1] * r * __ldg(g + c0 + 2 * e + 1));
+      __nv_bfloat162 hh = __floats2bfloat162_rn(v[i][2 * e] * r * gg[2 * e],
+                                                v[i][2 * e + 1] * r * gg[2 * e + 1]);
       w[e] = *reinterpret_cast<uint32_t *>(&hh);
     }
     o[i * 32 + lane] = u;
@@ -382,46 +385,51 @@ __global__ void rmsnorm_bf16_kernel(const __nv_bfloat16 *__restrict__ in,
 // In place on the q and k heads of qkv rows: per-head RMSNorm (q_norm /
 // k_norm gammas) then rotary embedding (rotate-half convention) with the
 // precomputed table rope[p][i] = (cos, sin)(p * theta^(-2i/dh)), position
-// p = row % S. One warp per (row, head); dh/32 elements per lane, element j
-// pairs with j + dh/2 inside the same lane. (A vectorised variant with the
-// partner fetched by shuffle measured slower: 203 vs 143 us.)
+// p = row % S. One warp per token row, looping over its q and k heads (one
+// warp per (row, head) measured 143 us vs 93 us per config-4 layer); dh/32
+// elements per lane, element j pairs with j + dh/2 inside the same lane.
 template <int DH>
 __global__ void qk_norm_rope_kernel(__nv_bfloat16 *__restrict__ qkv, int64_t rows, int S, int Hq,
                                     int Hkv, const float *__restrict__ qg,
                                     const float *__restrict__ kg, float eps,
                                     const float2 *__restrict__ rope) {
   constexpr int E = DH / 32;
-  const int nh = Hq + Hkv;
-  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (item >= rows * nh) return;
-  const int64_t row = item / nh;
-  const int hd = (int)(item % nh);
+  if (row >= rows) return;  // one warp per token row, all q and k heads
   const int p = (int)(row % S);
-  const float *g = hd < Hq ? qg : kg;
-  __nv_bfloat16 *x = qkv + row * (int64_t)(Hq + 2 * Hkv) * DH + hd * DH;
-  float v[E];
-  float ss = 0.f;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    v[e] = __bfloat162float(x[e * 32 + lane]);
-    ss = fmaf(v[e], v[e], ss);
-  }
-  const float r = rsqrtf(warp_sum(ss) / DH + eps);
-#pragma unroll
-  for (int e = 0; e < E; ++e) v[e] *= r * __ldg(g + e * 32 + lane);
   const float2 *rp = rope + (size_t)p * (DH / 2);
-  float o[E];
+  float2 cs[E];
+  float gq[E], gk[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int j = e * 32 + lane;
-    const float2 cs = __ldg(rp + j % (DH / 2));
-    const int pe = e < E / 2 ? e + E / 2 : e - E / 2;  // partner j +- dh/2
-    const float rot = e < E / 2 ? -v[pe] : v[pe];
-    o[e] = fmaf(v[e], cs.x, rot * cs.y);
+    cs[e] = __ldg(rp + j % (DH / 2));
+    gq[e] = __ldg(qg + j);
+    gk[e] = __ldg(kg + j);
   }
+  __nv_bfloat16 *base = qkv + row * (int64_t)(Hq + 2 * Hkv) * DH;
+#pragma unroll 2
+  for (int hd = 0; hd < Hq + Hkv; ++hd) {
+    __nv_bfloat16 *x = base + hd * DH;
+    const bool isq = hd < Hq;
+    float v[E];
+    float ss = 0.f;
 #pragma unroll
-  for (int e = 0; e < E; ++e) x[e * 32 + lane] = __float2bfloat16_rn(o[e]);
+    for (int e = 0; e < E; ++e) {
+      v[e] = __bfloat162float(x[e * 32 + lane]);
+      ss = fmaf(v[e], v[e], ss);
+    }
+    const float r = rsqrtf(warp_sum(ss) / DH + eps);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] *= r * (isq ? gq[e] : gk[e]);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int pe = e < E / 2 ? e + E / 2 : e - E / 2;  // partner j +- dh/2
+      const float rot = e < E / 2 ? -v[pe] : v[pe];
+      x[e * 32 + lane] = __float2bfloat16_rn(fmaf(v[e], cs[e].x, rot * cs[e].y));
+    }
+  }
 }
 
 // Last-token pooling: final RMSNorm of row S-1 of each sequence, then L2
@@ -881,7 +889,7 @@ int forward_decoder(lv_encoder *e, const void *tokens, int token_bytes, int S,
       rmsnorm_bf16_kernel<<<rn_blocks, 256, 0, s>>>(cur, tmp, L.ln1_g, M, d, c.norm_eps);
       note_launch();
       LV_TRY(gemm<bf>(e, tmp, L.w_qkv, e->zeros, nullptr, qkv, M, nqkv, d, EPI_BIAS, s));
-      const int64_t items = (int64_t)M * (Hq + Hk);
+      const int64_t items = M;  // one warp per token row
       if (dh == 128)
         qk_norm_rope_kernel<128><<<(unsigned)((items + 7) / 8), 256, 0, s>>>(
             qkv, M, S, Hq, Hk, L.qn_g, L.kn_g, c.norm_eps, e->rope);
