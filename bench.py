@@ -282,11 +282,11 @@ def cpu_sample(W, cfg, args, ef, qi, budget_s, r_total):
     `budget_s` seconds. Returns (seconds, fraction of the query completed)."""
     import torch
     from oracle import search_port as sp
-    from oracle.encoder_ref import RefEncoder
+    from oracle.encoder_ref import make_ref_encoder
     g = W["graph"]
     og = sp.CsrGraph(g.n, g.max_degree, g.entry_point, g.levels, g.level_offsets,
                      g.level_neighbors)
-    ref = W.setdefault("_ref_enc", RefEncoder(W["ecfg"], W["weights"]))
+    ref = W.setdefault("_ref_enc", make_ref_encoder(W["ecfg"], W["weights"]))
     t0 = time.perf_counter()
     q = ref.encode(W["qtokens"][qi:qi + 1].astype(np.int64))[0]   # embed_query
     src = _CpuEncoderSource(ref, W["tokens"], budget_s)
