@@ -544,15 +544,25 @@ def main():
     if est["attn_ms"]:
         na = max(1, est["attn_launches"])
         attn_gbs = est["attn_bytes"] / (est["attn_ms"] / 1e3) / 1e9
-        rooflines.append({
-            "kernel": "attn_tc_kernel (tcgen05 Q.K^T -> TMEM softmax -> P.V)", "bound": "hbm",
-            "achieved": round(attn_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(attn_gbs / peaks["hbm_gbs"], 4),
-            "traffic": traffic.get("attn_tc_kernel"), "peak_source": peaks_kind,
-            "algorithmic_bytes_per_launch": est["attn_bytes"] / na,
-            "tensor_tflops": round(est["attn_flops"] / (est["attn_ms"] / 1e3) / 1e12, 1),
-            "launches": est["attn_launches"],
-            "share_of_step": round(est["attn_ms"] / ms, 4) if ms else None})
+        attn_tf = est["attn_flops"] / (est["attn_ms"] / 1e3) / 1e12
+        if getattr(W["ecfg"], "arch", 0) == 1:   # config-4: causal GQA, compute-side bound
+            rooflines.append({
+                "kernel": "attn_tc_causal_kernel (tcgen05 causal GQA, two-pass softmax)",
+                "bound": "tensor", "achieved": round(attn_tf, 1), "peak": gemm_peak,
+                "unit": "TFLOP/s", "frac": round(attn_tf / gemm_peak, 4),
+                "traffic": traffic.get("attn_tc_causal_kernel"),
+                "peak_source": f"{peaks_kind} bf16 sustained", "hbm_gbs": round(attn_gbs, 1),
+                "launches": est["attn_launches"],
+                "share_of_step": round(est["attn_ms"] / ms, 4) if ms else None})
+        else:
+            rooflines.append({
+                "kernel": "attn_tc_kernel (tcgen05 Q.K^T -> TMEM softmax -> P.V)", "bound": "hbm",
+                "achieved": round(attn_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(attn_gbs / peaks["hbm_gbs"], 4),
+                "traffic": traffic.get("attn_tc_kernel"), "peak_source": peaks_kind,
+                "algorithmic_bytes_per_launch": est["attn_bytes"] / na,
+                "tensor_tflops": round(attn_tf, 1), "launches": est["attn_launches"],
+                "share_of_step": round(est["attn_ms"] / ms, 4) if ms else None})
     rooflines.append({
         "kernel": "frontier_kernel (CSR gather + ADC + AQ/EQ + exact scoring)", "bound": "hbm",
         "achieved": round(frontier_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",

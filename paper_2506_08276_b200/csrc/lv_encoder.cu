@@ -733,20 +733,26 @@ int fused_gemm(lv_encoder *e, const void *A, const void *W, const void *res, voi
 
 // bf16 attention with optional CUDA-event timing (profile mode): algorithmic
 // work 4*S^2*dh*H FLOPs and qkv + context bytes per sequence
+// Hkv > 0: grouped-query causal attention (decoder-style encoder, causal
+// FLOPs counted at half); bytes = q, k, v read + context written.
 int timed_attention(lv_encoder *e, const __nv_bfloat16 *qkv, __nv_bfloat16 *ctx, int ns, int S,
-                    int H, int dh, cudaStream_t s) {
+                    int H, int dh, cudaStream_t s, int Hkv = 0) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (e->profile) {
     e0 = take_event(e);
     e1 = take_event(e);
     cudaEventRecord(e0, s);
   }
-  LV_CHECK_CUDA(attention_bf16(qkv, ctx, ns, S, H, dh, s));
+  if (Hkv > 0)
+    LV_CHECK_CUDA(attention_gqa_bf16(qkv, ctx, ns, S, H, Hkv, dh, true, s));
+  else
+    LV_CHECK_CUDA(attention_bf16(qkv, ctx, ns, S, H, dh, s));
   if (e->profile) {
     cudaEventRecord(e1, s);
     e->ev_used.emplace_back(e0, e1);
-    e->ev_flops.push_back(4.0 * ns * (double)S * S * dh * H);
-    e->ev_bytes.push_back(2.0 * ns * (double)S * 4 * H * dh);
+    const double heads_io = Hkv > 0 ? 2.0 * H + 2.0 * Hkv : 4.0 * H;
+    e->ev_flops.push_back((Hkv > 0 ? 2.0 : 4.0) * ns * (double)S * S * dh * H);
+    e->ev_bytes.push_back(2.0 * ns * (double)S * heads_io * dh);
     e->ev_kind.push_back(1);
   }
   return LV_OK;
@@ -897,7 +903,7 @@ int forward_decoder(lv_encoder *e, const void *tokens, int token_bytes, int S,
         qk_norm_rope_kernel<64><<<(unsigned)((items + 7) / 8), 256, 0, s>>>(
             qkv, M, S, Hq, Hk, L.qn_g, L.kn_g, c.norm_eps, e->rope);
       note_launch();
-      LV_CHECK_CUDA(attention_gqa_bf16(qkv, ctx, (int)ns, S, Hq, Hk, dh, true, s));
+      LV_TRY(timed_attention(e, qkv, ctx, (int)ns, S, Hq, dh, s, Hk));
       LV_TRY(gemm<bf>(e, ctx, L.w_o, e->zeros, cur, tmp, M, d, Hq * dh, EPI_BIAS_RESIDUAL, s));
       std::swap(cur, tmp);
       rmsnorm_bf16_kernel<<<rn_blocks, 256, 0, s>>>(cur, tmp, L.ln2_g, M, d, c.norm_eps);
