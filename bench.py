@@ -336,7 +336,7 @@ def main():
     args = ap.parse_args()
     args.pool = 0
     cfg = dict(CONFIGS[args.config])
-    args.alphas = [float(x) for x in (args.alphas or cfg.get("alphas", "30,50,70,80,90,100")).split(",")]
+    args.alphas = [float(x) for x in (args.alphas or cfg.get("alphas", "30,50,60,65,70,75,80,90,100")).split(",")]
     args.alpha = args.alphas[0]
     args.pool = (args.batch or cfg["batch"]) * int(os.environ.get("WORLD_SIZE", "1"))
     if args.n:

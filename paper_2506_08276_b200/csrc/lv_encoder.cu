@@ -313,7 +313,8 @@ __global__ void pool_ln_kernel(const __nv_bfloat16 *__restrict__ y, const float2
 __global__ void embed_gather_kernel(const void *__restrict__ tokens, int token_bytes, int S,
                                     const int32_t *__restrict__ ids, int64_t seq0, int64_t n_seqs,
                                     const float *__restrict__ tok_emb, int vocab, int d,
-                                    __nv_bfloat16 *__restrict__ out) {
+                                    __nv_bfloat16 *__restrict__ out,
+                                    float2 *__restrict__ st = nullptr, float eps = 0.f) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n_seqs * S) return;
@@ -326,14 +327,36 @@ __global__ void embed_gather_kernel(const void *__restrict__ tokens, int token_b
   if (tok >= (uint32_t)vocab) tok = vocab - 1;
   const float4 *te = reinterpret_cast<const float4 *>(tok_emb + (size_t)tok * d);
   uint2 *o = reinterpret_cast<uint2 *>(out + row * d);
+  float ss = 0.f;  // sum of squares of the stored (bf16) values
   for (int c = lane; c < d / 4; c += 32) {
     const float4 v = __ldg(te + c);
     uint2 u;
     __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+    ss = fmaf(fa.x, fa.x, fmaf(fa.y, fa.y, fmaf(fb.x, fb.x, fmaf(fb.y, fb.y, ss))));
     u.x = *reinterpret_cast<uint32_t *>(&a);
     u.y = *reinterpret_cast<uint32_t *>(&b);
     o[c] = u;
   }
+  if (st) {  // RMSNorm statistics (mean 0, rstd) of the row for the folded consumer GEMM
+    ss = warp_sum(ss);
+    if (lane == 0) st[row] = make_float2(0.f, rsqrtf(ss / d + eps));
+  }
+}
+
+// RMSNorm statistics from the per-64-column-box (mean, M2) partials of an
+// EPF_STATS epilogue: (0, rsqrt(mean(x^2) + eps)), one thread per row.
+__global__ void rms_stats_finalize_kernel(const float2 *__restrict__ parts, int nbox, float eps,
+                                          float2 *__restrict__ out, int64_t rows) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const float2 *p = parts + r * nbox;
+  float ss = 0.f;
+  for (int b = 0; b < nbox; ++b) {
+    const float2 t = __ldg(p + b);
+    ss += fmaf(64.f * t.x, t.x, t.y);
+  }
+  out[r] = make_float2(0.f, rsqrtf(ss / (64.f * nbox) + eps));
 }
 
 // out = x * rsqrt(mean(x^2) + eps) * g (RMSNorm), bf16 rows, one warp per row,
@@ -538,6 +561,8 @@ struct EncLayer {
 struct DecLayer {
   float *ln1_g = nullptr, *qn_g = nullptr, *kn_g = nullptr, *ln2_g = nullptr;
   void *w_qkv = nullptr, *w_o = nullptr, *w_gu = nullptr /* [gate; up] */, *w_down = nullptr;
+  // RMSNorm gammas folded into the consuming weights (fused mode): W diag(g)
+  void *w_qkv_f = nullptr, *w_gu_f = nullptr;
 };
 
 struct lv_encoder {
@@ -887,11 +912,59 @@ int forward_decoder(lv_encoder *e, const void *tokens, int token_bytes, int S,
     const int M = (int)(ns * S);
     cur = (bf *)e->x;
     tmp = (bf *)e->y;
+    const bool fuse = e->fuse_ln;
     embed_gather_kernel<<<(unsigned)((M + 7) / 8), 256, 0, s>>>(
-        tokens, token_bytes, S, d_ids, s0, ns, e->tok_emb, c.vocab, d, cur);
+        tokens, token_bytes, S, d_ids, s0, ns, e->tok_emb, c.vocab, d, cur,
+        fuse ? e->st2 : nullptr, c.norm_eps);
     note_launch();
     const unsigned rn_blocks = (unsigned)((M + 7) / 8);
+    if (fuse) {
+      // RMSNorms folded: producers emit row statistics, consumers use gamma-
+      // scaled weights and scale their accumulators by rstd (EPF_LN_IN, mean 0)
+      auto rms_final = [&](float2 *dst) -> int {
+        rms_stats_finalize_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(
+            e->st_part, d / 64, c.norm_eps, dst, M);
+        note_launch();
+        LV_CHECK_CUDA(cudaGetLastError());
+        return LV_OK;
+      };
+      for (const DecLayer &L : e->dec) {
+        EpiParams q;
+        q.bias = e->zeros;
+        q.colc = e->zeros;
+        q.ln_in = e->st2;
+        q.flags = EPF_LN_IN;
+        LV_TRY(fused_gemm(e, cur, L.w_qkv_f, nullptr, qkv, M, nqkv, d, q, s));
+        if (dh == 128)
+          qk_norm_rope_kernel<128><<<rn_blocks, 256, 0, s>>>(qkv, M, S, Hq, Hk, L.qn_g, L.kn_g,
+                                                              c.norm_eps, e->rope);
+        else
+          qk_norm_rope_kernel<64><<<rn_blocks, 256, 0, s>>>(qkv, M, S, Hq, Hk, L.qn_g, L.kn_g,
+                                                             c.norm_eps, e->rope);
+        note_launch();
+        LV_TRY(timed_attention(e, qkv, ctx, (int)ns, S, Hq, dh, s, Hk));
+        EpiParams o;
+        o.bias = e->zeros;
+        o.flags = EPF_RES | EPF_STATS;
+        o.stats = e->st_part;
+        LV_TRY(fused_gemm(e, ctx, L.w_o, cur, tmp, M, d, Hq * dh, o, s));
+        std::swap(cur, tmp);
+        LV_TRY(rms_final(e->st1));
+        EpiParams sg;
+        sg.flags = EPF_SWIGLU | EPF_LN_IN;
+        sg.ln_in = e->st1;
+        LV_TRY(fused_gemm(e, cur, L.w_gu_f, nullptr, gu, M, 2 * ff, d, sg, s));
+        EpiParams dn;
+        dn.bias = e->zeros;
+        dn.flags = EPF_RES | EPF_STATS;
+        dn.stats = e->st_part;
+        LV_TRY(fused_gemm(e, gu, L.w_down, cur, tmp, M, d, ff, dn, s));
+        std::swap(cur, tmp);
+        LV_TRY(rms_final(e->st2));
+      }
+    }
     for (const DecLayer &L : e->dec) {
+      if (fuse) break;
       rmsnorm_bf16_kernel<<<rn_blocks, 256, 0, s>>>(cur, tmp, L.ln1_g, M, d, c.norm_eps);
       note_launch();
       LV_TRY(gemm<bf>(e, tmp, L.w_qkv, e->zeros, nullptr, qkv, M, nqkv, d, EPI_BIAS, s));
@@ -1020,7 +1093,17 @@ int create_decoder(const lv_encoder_config *cfg_in, const float *const *weights,
     }
     if (rc == LV_OK) rc = upload_mat(e, &L.w_gu, gu.data(), 2 * ff * d);
     upm(&L.w_down, b + 8, d * ff);
+    // folded copies: columns scaled by the RMSNorm gamma of their input
+    const float *g1 = weights[b + 0], *g2 = weights[b + 5];
+    std::vector<float> wq((size_t)nqkv * d);
+    for (size_t n = 0; n < (size_t)nqkv; ++n)
+      for (size_t k = 0; k < d; ++k) wq[n * d + k] = weights[b + 1][n * d + k] * g1[k];
+    if (rc == LV_OK) rc = upload_mat(e, &L.w_qkv_f, wq.data(), wq.size());
+    for (size_t n = 0; n < 2 * ff; ++n)
+      for (size_t k = 0; k < d; ++k) gu[n * d + k] *= g2[k];
+    if (rc == LV_OK) rc = upload_mat(e, &L.w_gu_f, gu.data(), 2 * ff * d);
   }
+  e->fuse_ln = rc == LV_OK;
   up(&e->final_g, 1 + 9 * cfg.layers, d);
   if (rc == LV_OK) {
     const size_t nz = std::max<size_t>(std::max<size_t>(nqkv, 2 * ff), d);
@@ -1231,7 +1314,9 @@ int lv_set_gemm_mode(int mode) {
 
 int lv_encoder_set_fused_ln(lv_encoder *enc, int enable) {
   LV_REQUIRE(enc, LV_ERR_USAGE, "null encoder");
-  const bool can = enc->cfg.precision == 1 && !enc->layers.empty() && enc->layers[0].w_1_f;
+  const bool can = enc->cfg.precision == 1 &&
+                   ((!enc->layers.empty() && enc->layers[0].w_1_f) ||
+                    (!enc->dec.empty() && enc->dec[0].w_qkv_f));
   LV_REQUIRE(!enable || can, LV_ERR_USAGE,
              "fused LayerNorm needs the bf16 encoder with hidden, ffn % 256 == 0");
   enc->fuse_ln = enable != 0;

@@ -553,6 +553,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int tile = pair; tile < num_tiles; tile += n_pairs) {
       const int y = (tile / n_tiles) * 256 + (int)rank * 128 + q * 32;
       const int xo = (tile % n_tiles) * (BN / 2) + half * 64;
+      float rs = 1.f;  // RMSNorm folded in (EPF_LN_IN, mean 0): silu(rs g) * (rs u)
+      if ((ep.flags & EPF_LN_IN) && y + lane < M) rs = __ldg(ep.ln_in + y + lane).y;
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
       if (lane == 0) bulk_wait_read<0>();  // the previous tile's store has read the box
@@ -575,10 +577,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float g0 = __uint_as_float(g[8 * k + 2 * e]), g1 = __uint_as_float(g[8 * k + 2 * e + 1]);
+            const float g0 = rs * __uint_as_float(g[8 * k + 2 * e]);
+            const float g1 = rs * __uint_as_float(g[8 * k + 2 * e + 1]);
             const float s0 = __fdividef(g0, 1.f + __expf(-g0)), s1 = __fdividef(g1, 1.f + __expf(-g1));
-            w[e] = pack_bf16(s0 * __uint_as_float(u[8 * k + 2 * e]),
-                             s1 * __uint_as_float(u[8 * k + 2 * e + 1]));
+            w[e] = pack_bf16(s0 * rs * __uint_as_float(u[8 * k + 2 * e]),
+                             s1 * rs * __uint_as_float(u[8 * k + 2 * e + 1]));
           }
           *reinterpret_cast<uint4 *>(box + row_off + (((uint32_t)(c * 4 + k) ^ sw) << 4)) =
               make_uint4(w[0], w[1], w[2], w[3]);
@@ -938,12 +941,12 @@ int tc_gemm_ex(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloat
              "tc_gemm_ex: need N % 256 == 0 and K % 64 == 0");
   LV_REQUIRE(ep.bias != nullptr || (ep.flags & EPF_SWIGLU), LV_ERR_USAGE,
              "tc_gemm_ex: bias required");
-  LV_REQUIRE(!(ep.flags & EPF_SWIGLU) || ep.flags == EPF_SWIGLU, LV_ERR_USAGE,
-             "tc_gemm_ex: the SwiGLU epilogue combines with no other flag");
+  LV_REQUIRE(!(ep.flags & EPF_SWIGLU) || (ep.flags & ~(EPF_SWIGLU | EPF_LN_IN)) == 0,
+             LV_ERR_USAGE, "tc_gemm_ex: the SwiGLU epilogue combines only with LN-in");
   LV_REQUIRE(!(ep.flags & EPF_RES) || residual != nullptr, LV_ERR_USAGE,
              "tc_gemm_ex: residual required");
-  LV_REQUIRE(!(ep.flags & EPF_LN_IN) || (ep.colc && ep.ln_in), LV_ERR_USAGE,
-             "tc_gemm_ex: LN-in needs colc and row statistics");
+  LV_REQUIRE(!(ep.flags & EPF_LN_IN) || (ep.ln_in && (ep.colc || (ep.flags & EPF_SWIGLU))),
+             LV_ERR_USAGE, "tc_gemm_ex: LN-in needs colc and row statistics");
   LV_REQUIRE(!(ep.flags & EPF_RES_LN) || (ep.res_ln && ep.res_g && ep.res_b), LV_ERR_USAGE,
              "tc_gemm_ex: residual LN needs statistics and affine");
   LV_REQUIRE(!(ep.flags & EPF_STATS) || ep.stats, LV_ERR_USAGE, "tc_gemm_ex: stats buffer");

@@ -295,10 +295,6 @@ class DeviceIndex:
         if isinstance(source, MatrixSource):
             p.source = _lib.LV_SOURCE_MATRIX
             self.set_matrix(source.matrix)
-        elif isinstance(source, ProviderSource) and dry_matrix is not None:
-            p.source = _lib.LV_SOURCE_ENCODER
-            p.flags |= _lib.LV_DRY_RECOMPUTE
-            self.set_matrix(dry_matrix)
         elif isinstance(source, ProviderSource):
             p.source = _lib.LV_SOURCE_ENCODER
             self.attach_encoder(source.provider)

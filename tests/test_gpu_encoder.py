@@ -230,6 +230,27 @@ def test_decoder_encoder_close_to_torch(lv, name, S):
     assert cos.min() > 0.99, cos
 
 
+@pytest.mark.parametrize("name,S", [("dh64", 128), ("qwen3", 512)])
+def test_decoder_fused_rmsnorm_matches_unfused(lv, name, S):
+    """RMSNorms folded into the GEMMs (row statistics from the producing GEMM
+    or the embedding gather, gamma folded into the consuming weights, rstd in
+    the epilogue — including the SwiGLU epilogue) match standalone RMSNorm
+    kernels up to bf16 rounding."""
+    from oracle.encoder_ref import make_ref_encoder
+    from paper_2506_08276_b200.encoder import GpuEncoder, init_weights, synthetic_tokens
+    cfg = _dec_cfg(name)
+    w = init_weights(cfg, seed=41)
+    tok = synthetic_tokens(4, S, cfg.vocab, seed=42)
+    enc = GpuEncoder(cfg, w, precision="bf16")
+    fused = enc.encode(tok)
+    enc.set_fused_layernorm(False)
+    plain = enc.encode(tok)
+    ref = make_ref_encoder(cfg, w).encode(tok.astype(np.int64))
+    cos = lambda a, b: (a * b).sum(1) / np.linalg.norm(a, axis=1) / np.linalg.norm(b, axis=1)
+    assert cos(fused, plain).min() > 0.998, cos(fused, plain)
+    assert cos(fused, ref).min() > 0.99, cos(fused, ref)
+
+
 def test_decoder_encoder_batch_invariant(lv):
     from paper_2506_08276_b200.encoder import GpuEncoder, init_weights, synthetic_tokens
     cfg = _dec_cfg("dh64")
