@@ -52,6 +52,14 @@ CONFIGS = {
                         "graph (M=32, m=6, beta=2%), PQ m=64, 4096-query pool, top-3",
                n=1_000_000, seq=256, encoder="bert-base", pq_m=64, k=3, n_queries=4096,
                batch=4096, corpus="lda"),
+    # config-3 (not the headline): 10M passages, PQ m=96; the builder switches to
+    # IVF approximate k-NN candidates above 2M nodes. Setup ~20 min (token
+    # generation on the host, 10M BERT-base embeddings, index build).
+    "c3": dict(workload="config-3: 10M passages x 256 tokens (LDA-style topic mixtures), "
+                        "BERT-base (768-d) random-init encoder, high-degree-preserving pruned "
+                        "graph (M=32, m=6, beta=2%), PQ m=96, 4096-query step, top-3",
+               n=10_000_000, seq=256, encoder="bert-base", pq_m=96, k=3, n_queries=4096,
+               batch=4096, corpus="lda"),
     # config-4 (not the headline): Qwen3-Embedding-0.6B-shaped decoder encoder
     # (arch 1, 481 GFLOP/passage), top-10, recompute-ratio sweep; use --n to
     # bound the corpus (embedding 1M x 512-token passages takes ~10 min)

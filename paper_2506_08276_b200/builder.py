@@ -50,6 +50,7 @@ class GpuBuildParams:
     pq_subspaces: int | None = None
     pq_iters: int = 10
     candidates: int = 64      # k-NN pool per node (plays ef_construction's role)
+    exact_knn_max: int = 2_000_000  # above: IVF approximate k-NN (_knn_ivf)
 
     def __post_init__(self) -> None:
         if self.low_degree is None:
@@ -88,7 +89,7 @@ def _pair_dist(a, b, metric):
     return -(a * b).sum(-1)
 
 
-def _knn(x, k: int, metric: str, chunk: int = 2048):
+def _knn(x, k: int, metric: str, chunk: int = 0):
     """Exact k nearest (excluding self) of every row of x among x: bf16 GEMM
     candidates (k + 16 of them), re-ranked with fp32 distances.
 
@@ -111,6 +112,7 @@ def _knn(x, k: int, metric: str, chunk: int = 2048):
     ids = torch.empty((n, kk), dtype=torch.int64, device=x.device)
     dist = torch.empty((n, kk), dtype=torch.float32, device=x.device)
     ar = torch.arange(n, device=x.device)
+    chunk = chunk or max(256, min(2048, (1 << 31) // max(1, n)))  # <= 8 GB of scores
     for s in range(0, n, chunk):
         e = min(n, s + chunk)
         sc = (xb[s:e] @ xb.T).float()
@@ -127,6 +129,81 @@ def _knn(x, k: int, metric: str, chunk: int = 2048):
         order = torch.argsort(dd, dim=1, stable=True)
         ids[s:e] = cand.gather(1, order)[:, :kk]
         dist[s:e] = dd.gather(1, order)[:, :kk]
+    return ids, dist
+
+
+def _rerank(x, rows, cand, kk, metric):
+    """Exact fp32 distances of candidate ids ``cand`` [b, c] to rows ``rows``
+    [b] (self excluded), sorted by (distance, id); the first kk kept."""
+    import torch
+    dd = _pair_dist(x[rows][:, None, :], x[cand], metric)
+    dd = torch.where(cand == rows[:, None], torch.full_like(dd, float("inf")), dd)
+    order = torch.argsort(cand, dim=1)
+    cand = cand.gather(1, order)
+    dd = dd.gather(1, order)
+    order = torch.argsort(dd, dim=1, stable=True)
+    return cand.gather(1, order)[:, :kk], dd.gather(1, order)[:, :kk]
+
+
+def _knn_ivf(x, k: int, metric: str, nlist: int = 0, nprobe: int = 8, sample: int = 262144,
+             iters: int = 8, seed: int = 0):
+    """Approximate k nearest of every row among x for corpora too large for the
+    exact O(n^2) scan (config-3: 10M): k-means (nlist ~ sqrt(n) centroids, on
+    a sample) over the mean-centred rows; every cluster's members search the
+    members of the cluster's nprobe nearest centroids (bf16 GEMM candidates,
+    exact fp32 re-rank as in _knn). Plays the role of the reference's
+    approximate HNSW candidate search (builder.py:285-366)."""
+    import torch
+    n, dim = x.shape
+    dev = x.device
+    kk = min(n - 1, k)
+    extra = kk + 16
+    nlist = nlist or 1 << max(4, int(round(math.log2(math.sqrt(n)))))
+    xc = x - x.mean(0, keepdim=True) if metric in ("cosine", "l2") else x
+    xb = xc.to(torch.bfloat16)
+    g = torch.Generator(device=dev).manual_seed(seed)
+    samp = xc[torch.randperm(n, generator=g, device=dev)[:min(n, sample)]]
+    cent = samp[:nlist].clone()
+
+    def nearest(v, c, chunk=65536):
+        cn = (c * c).sum(1)
+        out = torch.empty(v.shape[0], dtype=torch.int64, device=dev)
+        for s0 in range(0, v.shape[0], chunk):
+            out[s0:s0 + chunk] = (cn[None, :] - 2.0 * (v[s0:s0 + chunk].float() @ c.T)).argmin(1)
+        return out
+
+    for _ in range(iters):
+        a = nearest(samp, cent)
+        sums = torch.zeros_like(cent).index_add_(0, a, samp)
+        cnt = torch.bincount(a, minlength=nlist).float()
+        cent = torch.where(cnt[:, None] > 0, sums / cnt.clamp_min(1)[:, None], cent)
+    assign = nearest(xc, cent)
+    order = torch.argsort(assign)
+    counts = torch.bincount(assign, minlength=nlist)
+    starts = torch.cumsum(counts, 0) - counts
+    cc = (cent * cent).sum(1)
+    probe = (cc[None, :] - 2.0 * cent @ cent.T).topk(min(nprobe, nlist), dim=1,
+                                                     largest=False).indices
+    sq = (xb.float() ** 2).sum(1) if metric in ("cosine", "l2") else None
+    ids = torch.empty((n, kk), dtype=torch.int64, device=dev)
+    dist = torch.empty((n, kk), dtype=torch.float32, device=dev)
+    counts_h, starts_h, probe_h = counts.tolist(), starts.tolist(), probe.cpu().tolist()
+    for c in range(nlist):
+        if counts_h[c] == 0:
+            continue
+        q = order[starts_h[c]:starts_h[c] + counts_h[c]]
+        cand = torch.cat([order[starts_h[p]:starts_h[p] + counts_h[p]] for p in probe_h[c]])
+        for s0 in range(0, q.shape[0], 4096):
+            qq = q[s0:s0 + 4096]
+            sc = (xb[qq] @ xb[cand].T).float()
+            if sq is not None:
+                sc = 2 * sc - sq[cand][None, :]
+            sc[cand[None, :] == qq[:, None]] = -float("inf")
+            top = cand[sc.topk(min(extra, cand.shape[0]), dim=1).indices]
+            if top.shape[1] < kk:  # tiny neighbourhood: pad with self (rejected later)
+                top = torch.cat([top, qq[:, None].expand(-1, kk - top.shape[1])], 1)
+            ii, dd = _rerank(x, qq, top, kk, metric)
+            ids[qq], dist[qq] = ii, dd
     return ids, dist
 
 
@@ -234,7 +311,8 @@ def build_graph_gpu(matrix, params: GpuBuildParams) -> PrunedGraph:
     base = torch.arange(n, device=dev)
     full_caps = torch.full((n,), M, dtype=torch.int32, device=dev)
     # pass 1 (uniform cap) -> degrees -> hubs
-    knn0 = _knn(x, params.candidates, params.metric)
+    knn0 = (_knn(x, params.candidates, params.metric) if n <= params.exact_knn_max
+            else _knn_ivf(x, params.candidates, params.metric, seed=params.seed))
     offs1, _ = _level_graph(x, base, full_caps, M, params.metric, params.candidates, knn0)
     degrees = np.diff(offs1.astype(np.int64))
     hubs = select_hubs(degrees, params.hub_percent, n)
@@ -312,7 +390,7 @@ def train_pq_gpu(matrix, m_pq: int | None, metric: str, iters: int = 10, seed: i
     return model, PQCodes(codes=codes.cpu().numpy())
 
 
-def brute_force_topk(matrix, queries, k: int, metric: str, deleted=None, chunk: int = 1024):
+def brute_force_topk(matrix, queries, k: int, metric: str, deleted=None, chunk: int = 0):
     """evaluation.py:82-95 on the GPU in fp32: k smallest (distance, id) over active rows."""
     import torch
     prev = torch.backends.cuda.matmul.allow_tf32
@@ -320,6 +398,7 @@ def brute_force_topk(matrix, queries, k: int, metric: str, deleted=None, chunk: 
     try:
         E = matrix.float()
         Q = torch.as_tensor(queries, dtype=torch.float32, device=E.device)
+        chunk = chunk or max(16, min(1024, (1 << 31) // max(1, E.shape[0])))  # <= 8 GB of scores
         if metric == "cosine":
             rn = E.norm(dim=1)
         out = np.empty((Q.shape[0], k), dtype=np.int64)
