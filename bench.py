@@ -341,12 +341,18 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--batch-sweep", default="",
+                    help="also time one step at each of these concurrent-query counts "
+                         "(config-5 style), e.g. 256,1024,4096,16384")
     args = ap.parse_args()
     args.pool = 0
     cfg = dict(CONFIGS[args.config])
     args.alphas = [float(x) for x in (args.alphas or cfg.get("alphas", "30,50,60,65,70,75,80,90,100")).split(",")]
     args.alpha = args.alphas[0]
     args.pool = (args.batch or cfg["batch"]) * int(os.environ.get("WORLD_SIZE", "1"))
+    args.sweep = [int(x) for x in args.batch_sweep.split(",") if x]
+    if args.sweep:
+        args.pool = max(args.pool, max(args.sweep))
     if args.n:
         cfg["n"] = args.n
         cfg["workload"] += f" [corpus reduced to n={args.n} for profiling]"
@@ -603,9 +609,39 @@ def main():
         "roofline": roofline, "rooflines": rooflines,
         "clocks": clocks, "gpu_launches": launches_all, "e2e": e2e,
     }
+    if args.sweep and world == 1:
+        line["batch_sweep"] = batch_sweep(W, cfg, args, dev_index, params, source, hub_cache)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(W, cfg, args, ef, out_buf, all_idx[-1])
     print(json.dumps(line), flush=True)
+
+
+def batch_sweep(W, cfg, args, dev_index, params, source, hub_cache):
+    """Config-5-style sweep: one timed step (query encoding + recompute search,
+    CUDA events) per concurrent-query count B, at the tuned (ef, rerank%).
+    Workspaces for B are sized first by a dry recompute search (untimed)."""
+    import torch
+    import paper_2506_08276_b200 as lv
+    out = []
+    for B in args.sweep:
+        qt = W["qtok_dev"][:B].contiguous()
+        dev_index.search_device(W["Q"][:B].contiguous(), params, lv.ProviderSource(W["prov"]),
+                                cache=hub_cache, dry_matrix=W["E"], max_inflight=B)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        Qb = W["enc"].encode(qt)
+        res = dev_index.search_device(Qb, params, source, cache=hub_cache, max_inflight=B)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        st = dev_index.last_stats()
+        rec = recall_of(res["ids"][:B].cpu().numpy(), W["gt"][:B])
+        out.append({"concurrent_queries": B, "queries_per_s": round(B / (ms / 1e3), 2),
+                    "physical_per_query": round(st["physical_encodes"] / B, 1),
+                    "recall_at_3": round(rec, 4), "ms": round(ms, 1)})
+        log(f"sweep: B={B} {out[-1]}")
+    return out
 
 
 def cpu_baseline(W, cfg, args, ef, out_buf, last_idx):
