@@ -13,6 +13,7 @@
 //   adc_build                    pq.py:153-178       (lut_kernel)
 //   approx_distance_many         pq.py:186-189       (adc_one, lv_numerics.cuh)
 //   distance_many                vectors.py:120-140  (resolve / dist_kernel)
+#include <algorithm>
 #include "lv_search.cuh"
 #include "lv_numerics.cuh"
 
@@ -617,6 +618,30 @@ __global__ void adc_score_kernel(const float *__restrict__ lut, int m,
   out[i] = adc_one(lut, codes + ids[i] * m, m);
 }
 
+// Streaming ADC (approx_distance_many, pq.py:186-189) over many ids of one
+// query: the query's LUT is staged in shared memory once per CTA (persistent
+// grid), each thread reads its node's m code bytes with 16-byte loads (one
+// 64-byte line at m = 64) and sums the LUT entries in numpy's fp64 pairwise
+// order — bit-identical to adc_one.
+template <int M>
+__global__ void __launch_bounds__(256) adc_stream_kernel(const float *__restrict__ lut,
+                                                         const uint8_t *__restrict__ codes,
+                                                         const int64_t *__restrict__ ids,
+                                                         int64_t count, float *__restrict__ out) {
+  extern __shared__ float slut[];
+  for (int i = threadIdx.x; i < M * 256; i += blockDim.x) slut[i] = lut[i];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 *cp = reinterpret_cast<const uint4 *>(codes + __ldg(ids + i) * M);
+    uint8_t c[M];
+#pragma unroll
+    for (int v = 0; v < M / 16; ++v) *reinterpret_cast<uint4 *>(c + 16 * v) = __ldg(cp + v);
+    auto get = [&](int s) -> double { return (double)slut[s * 256 + c[s]]; };
+    out[i] = __double2float_rn(pairwise_sum(get, M));
+  }
+}
+
 __global__ void dist_kernel(int metric, const float *__restrict__ rows, int64_t nrows, int dim,
                             const float *__restrict__ q, float qn, float *__restrict__ out) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -746,9 +771,29 @@ cudaError_t launch_lut(const float *q, const float *qn, int B, int dim, int metr
   return cudaGetLastError();
 }
 
+template <int M>
+cudaError_t launch_adc_stream(const float *lut, const uint8_t *codes, const int64_t *ids,
+                              int64_t count, float *out, cudaStream_t s) {
+  const int smem = M * 256 * 4;
+  cudaError_t e =
+      cudaFuncSetAttribute(adc_stream_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)sms * (M <= 64 ? 3 : 2));
+  adc_stream_kernel<M><<<(unsigned)blocks, 256, smem, s>>>(lut, codes, ids, count, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_adc_score(const float *lut, int m, const uint8_t *codes, const int64_t *ids,
                              int64_t count, float *out, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
+  const bool aligned = ((uintptr_t)codes & 15) == 0;
+  if (aligned && m == 32) return launch_adc_stream<32>(lut, codes, ids, count, out, s);
+  if (aligned && m == 64) return launch_adc_stream<64>(lut, codes, ids, count, out, s);
+  if (aligned && m == 96) return launch_adc_stream<96>(lut, codes, ids, count, out, s);
   adc_score_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(lut, m, codes, ids, count, out);
   note_launch();
   return cudaGetLastError();
