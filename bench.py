@@ -191,6 +191,8 @@ def setup(cfg, args, device):
     log(f"index built in {time.time() - t1:.1f}s: levels={graph.level_count} "
         f"avg_deg={graph.out_degrees(0).mean():.2f}")
     gt = brute_force_topk(E, Q, cfg["k"], "cosine")
+    torch.cuda.empty_cache()  # the builder's cached blocks go back to the driver (the search
+    # library allocates with cudaMalloc; config-3 needs the room)
     return dict(ecfg=ecfg, weights=weights, enc=enc, tokens=tokens, qtokens=qtokens,
                 tok_dev=tok_dev, qtok_dev=qtok_dev, E=E, Q=Q, graph=graph, model=model,
                 codes=codes, gt=gt, setup_s=time.time() - t0, embed_s=embed_s, corpus=corpus)
