@@ -318,108 +318,6 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
-// Epilogue of one 32-column chunk of one row (shared by both kernels).
-__device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], const float *bias,
-                                               const __nv_bfloat16 *residual,
-                                               __nv_bfloat16 *out, int row, int gn, int N,
-                                               int epi) {
-  const float4 *b4 = reinterpret_cast<const float4 *>(bias + gn);
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    float4 bb = __ldg(b4 + j);
-    v[4 * j + 0] = __uint_as_float(r[4 * j + 0]) + bb.x;
-    v[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + bb.y;
-    v[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + bb.z;
-    v[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + bb.w;
-  }
-  if (epi == EPI_BIAS_GELU) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
-  } else if (epi == EPI_BIAS_RESIDUAL) {
-    const uint4 *rp = reinterpret_cast<const uint4 *>(residual + (size_t)row * N + gn);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      uint4 u = __ldg(rp + j);
-      const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float2 f = __bfloat1622float2(h[e]);
-        v[8 * j + 2 * e] += f.x;
-        v[8 * j + 2 * e + 1] += f.y;
-      }
-    }
-  }
-  uint4 *op = reinterpret_cast<uint4 *>(out + (size_t)row * N + gn);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint4 u;
-    u.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
-    u.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
-    u.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
-    u.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
-    op[j] = u;
-  }
-}
-
-// Per-chunk epilogue operands: 32 bias values and (residual epilogue) 32 bf16
-// residual values of the thread's row.
-struct EpiOperands {
-  float4 b[8];
-  uint4 res[4];
-};
-
-__device__ __forceinline__ void load_operands(EpiOperands &o, const float *bias,
-                                              const __nv_bfloat16 *residual, int row, int gn,
-                                              int N, int epi, bool live) {
-  const float4 *b4 = reinterpret_cast<const float4 *>(bias + gn);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) o.b[j] = __ldg(b4 + j);
-  if (epi == EPI_BIAS_RESIDUAL && live) {
-    const uint4 *rp = reinterpret_cast<const uint4 *>(residual + (size_t)row * N + gn);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) o.res[j] = __ldg(rp + j);
-  }
-}
-
-__device__ __forceinline__ void epilogue_apply(const uint32_t (&r)[32], const EpiOperands &o,
-                                               __nv_bfloat16 *out, int row, int gn, int N,
-                                               int epi) {
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    v[4 * j + 0] = __uint_as_float(r[4 * j + 0]) + o.b[j].x;
-    v[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + o.b[j].y;
-    v[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + o.b[j].z;
-    v[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + o.b[j].w;
-  }
-  if (epi == EPI_BIAS_GELU) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
-  } else if (epi == EPI_BIAS_RESIDUAL) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&o.res[j]);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float2 f = __bfloat1622float2(h[e]);
-        v[8 * j + 2 * e] += f.x;
-        v[8 * j + 2 * e + 1] += f.y;
-      }
-    }
-  }
-  uint4 *op = reinterpret_cast<uint4 *>(out + (size_t)row * N + gn);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint4 u;
-    u.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
-    u.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
-    u.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
-    u.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
-    op[j] = u;
-  }
-}
-
 template <int kMode>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
