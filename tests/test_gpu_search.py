@@ -164,3 +164,24 @@ def test_adc_kernels_bit_exact(lv, tag):
     assert np.array_equal(table.view(np.uint32), np.load(GOLDEN / f"adc_table_{tag}.npy").view(np.uint32))
     approx = dev.adc_score(table, np.arange(n))
     assert np.array_equal(approx.view(np.uint32), np.load(GOLDEN / f"adc_approx_{tag}.npy").view(np.uint32))
+
+
+@pytest.mark.parametrize("m", [32, 64, 96])
+def test_streaming_adc_bit_exact_vs_oracle(lv, m):
+    """lv_adc_score's streaming kernel (LUT in shared memory, 16-byte code
+    loads; m = 32/64/96) keeps numpy's fp64 pairwise order (pq.py:186-189)."""
+    from oracle.numerics import approx_distance_many
+    rng = np.random.default_rng(m)
+    n, dim = 5000, 768
+    cb = rng.standard_normal((m, 256, -(-dim // m)), dtype=np.float32)
+    model = lv.PQModel(dim=dim, padded_dim=cb.shape[2] * m, m_pq=m, metric="cosine", codebooks=cb)
+    codes = rng.integers(0, 256, (n, m), dtype=np.uint8)
+    g = lv.PrunedGraph(n=n, max_degree=1, entry_point=0, levels=np.zeros(n, np.uint16),
+                       level_offsets=[np.zeros(n + 1, np.uint64)],
+                       level_neighbors=[np.zeros(0, np.uint32)])
+    dev = lv.DeviceIndex(g, model, lv.PQCodes(codes))
+    table = (rng.standard_normal((m, 256)) * 0.1).astype(np.float32)
+    ids = rng.permutation(n)
+    got = dev.adc_score(table, ids)
+    ref = approx_distance_many(table, codes[ids])
+    assert np.array_equal(got.view(np.uint32), np.asarray(ref, dtype=np.float32).view(np.uint32))
