@@ -225,7 +225,8 @@ int lv_attention_gqa_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S,
 int lv_set_gemm_mode(int mode);
 /* Attention kernel selection: 0 = auto (tcgen05/TMEM kernel for dh == 64 and
  * S in {128, 256}, else the mma.sync kernel), 1 = mma.sync kernel only,
- * any other value = tcgen05 kernel where it applies. Returns the previous mode. */
+ * 2 = tcgen05 kernel with every third softmax exponential by polynomial on the FMA pipe
+ * (experiment), any other value = tcgen05 kernel where it applies. Returns the previous mode. */
 int lv_set_attention_mode(int mode);
 
 #ifdef __cplusplus
