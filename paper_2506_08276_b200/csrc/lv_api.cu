@@ -398,9 +398,17 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   if (enc_src) {
     LV_TRY(ws.greq.ensure(greq_cap));
     if (shared) {
-      // step-wide table of recomputed rows: <= 8 GiB, at least 4 iterations' worth
-      const int64_t budget = ((int64_t)8 << 30) / ((int64_t)ix->dim * 4);
-      tab_rows = std::max<int64_t>(greq_cap, std::min<int64_t>(budget, 16LL * greq_cap));
+      // step-wide table of recomputed rows (each distinct node is encoded once
+      // per call while the table has room; a full table is reset). Sized to
+      // hold every node when HBM allows — at 10M nodes and 16k queries in
+      // flight an 8 GiB table reset every few iterations and lost most of the
+      // sharing — keeping 12 GiB + 30% of the free memory for the encoder.
+      const int64_t row_bytes = (int64_t)ix->dim * 4;
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      const int64_t spare = std::max<int64_t>(0, ((int64_t)free_b - ((int64_t)12 << 30)) * 7 / 10);
+      const int64_t budget = std::max<int64_t>(((int64_t)8 << 30), spare) / row_bytes;
+      tab_rows = std::max<int64_t>(greq_cap, std::min<int64_t>(budget, ix->n));
       uint64_t hs = 1;
       while (hs < (uint64_t)(2 * tab_rows)) hs <<= 1;
       hmask = (uint32_t)(hs - 1);
