@@ -27,6 +27,11 @@
  *   lv_gemm_bf16         <- the dense contraction inside embed_batch (no reference
  *                           counterpart: the reference's provider is a hash, vectors.py:168-189);
  *                           exported for unit tests of the tcgen05 GEMM
+ *   lv_attention_bf16 / lv_attention_gqa_bf16
+ *                        <- the encoder's attention (BERT-style MHA; config-4 causal GQA),
+ *                           exported for unit tests of the tcgen05 attention kernels
+ *   lv_encoder_set_fused_ln, lv_set_gemm_mode, lv_set_attention_mode
+ *                        <- kernel-variant switches for parity tests and A/B measurements
  *
  * Conventions: plain pointers and sizes only. Unless LV_IO_DEVICE is set in a
  * call's flags, array arguments are HOST pointers and the call copies them
