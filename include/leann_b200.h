@@ -225,7 +225,9 @@ int lv_attention_gqa_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S,
                           int32_t Hkv, int32_t dh, int32_t causal, void *stream);
 /* GEMM kernel selection: 0 = auto (2-CTA cta_group::2 kernel when N % 256 == 0),
  * 1 = 1-CTA kernel only; + 2 = 3-buffer/3-stage epilogue for short-K residual GEMMs
- * (experiment; measured slower than the default 2-buffer/4-stage kernel).
+ * (experiment; measured slower than the default 2-buffer/4-stage kernel); + 4 = the
+ * 2-buffer/4-stage kernel also for long-K (K > 1024) residual GEMMs instead of the
+ * default 1-buffer/5-stage one.
  * Returns the previous mode. */
 int lv_set_gemm_mode(int mode);
 /* Attention kernel selection: 0 = auto (tcgen05/TMEM kernel for dh == 64 and

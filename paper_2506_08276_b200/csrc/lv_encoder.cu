@@ -1306,9 +1306,10 @@ int lv_attention_gqa_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S,
 }
 
 int lv_set_gemm_mode(int mode) {
-  const int prev = g_gemm_mode | (g_short_k != 0 ? 2 : 0);
+  const int prev = g_gemm_mode | (g_short_k != 0 ? 2 : 0) | (g_long_k_single ? 0 : 4);
   g_gemm_mode = mode & 1;
   g_short_k = (mode & 2) ? 1024 : 0;
+  g_long_k_single = (mode & 4) ? 0 : 1;
   return prev;
 }
 

@@ -28,6 +28,7 @@
 
 namespace lv {
 int g_short_k = 0;  // residual GEMMs with K <= this use the 3-buffer epilogue (off: measured slower)
+int g_long_k_single = 1;  // residual GEMMs with K > 1024: single box buffer, 5 stages (kMode 4)
 namespace {
 
 constexpr int kBM = 128;
@@ -268,9 +269,11 @@ constexpr int kColVecTotal = kEpiWarps * 2 * kColVecBytes;
 template <int kMode>
 struct PairCfg {
   // kMode 3: SwiGLU epilogue (no residual; gate/up interleaved per 64 columns)
-  static constexpr bool kRes = kMode == 1 || kMode == 2;
-  static constexpr int kStages = (kMode == 0 || kMode == 3) ? 5 : kMode == 1 ? 4 : 3;
-  static constexpr int kBufs = (kMode == 0 || kMode == 3) ? 1 : kMode == 1 ? 2 : 3;  // boxes per warp
+  // kMode 4: residual with a single box buffer and 5 stages (long-K GEMMs: the
+  // epilogue has slack, the residual box is loaded when the box starts)
+  static constexpr bool kRes = kMode == 1 || kMode == 2 || kMode == 4;
+  static constexpr int kStages = (kMode == 0 || kMode == 3 || kMode == 4) ? 5 : kMode == 1 ? 4 : 3;
+  static constexpr int kBufs = (kMode == 0 || kMode == 3 || kMode == 4) ? 1 : kMode == 1 ? 2 : 3;
   static constexpr int kStagingBytes = kEpiWarps * kBufs * kBoxBytes;
   static constexpr int kSmem = kStages * kStageBytes2 + kStagingBytes + kColVecTotal + 1024 + 512;
 };
@@ -609,7 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // next box's residual into the other buffer (its previous TMA store
         // must have finished reading it)
         if (lane == 0) {
-          if (has_res) {
+          if constexpr (kRes && kBufs > 1) {
             const int nt = b == 0 ? tile : tile + n_pairs;
             if (nt < num_tiles) {
               bulk_wait_read<kBufs - 2>();  // the store that last used buffer nb has read it
@@ -617,6 +620,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               box_coords(nt, b ^ 1, nx, ny);
               mbar_expect_tx(&rb[nb], kBoxBytes);
               tma_load_2d(stg + nb * kBoxBytes, &tmR, &rb[nb], nx, ny, pol_r);
+            }
+          } else if constexpr (kRes) {  // single buffer: this box's residual (box 0: prologue)
+            if (blk > 0) {
+              bulk_wait_read<0>();
+              mbar_expect_tx(&rb[0], kBoxBytes);
+              tma_load_2d(stg, &tmR, &rb[0], x, y, pol_r);
             }
           } else {
             bulk_wait_read<0>();  // the previous box's store has read the (single) buffer
@@ -782,12 +791,21 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<3>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<3>::kSmem));
+    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<4>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PairCfg<4>::kSmem));
     attr_set = true;
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = std::min(tiles, tc_gemm_num_sms() / 2);
-  const int mode = (ep.flags & EPF_SWIGLU) ? 3 : !(ep.flags & EPF_RES) ? 0 : (K <= g_short_k ? 2 : 1);
-  if (mode == 3)
+  const int mode = (ep.flags & EPF_SWIGLU) ? 3
+                   : !(ep.flags & EPF_RES) ? 0
+                   : K <= g_short_k ? 2
+                   : (K > 1024 && g_long_k_single) ? 4 : 1;
+  if (mode == 4)
+    tc_gemm_pair_kernel<4><<<2 * pairs, kThreads, PairCfg<4>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
+                                                                          ep);
+  else if (mode == 3)
     tc_gemm_pair_kernel<3><<<2 * pairs, kThreads, PairCfg<3>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
                                                                           ep);
   else if (mode == 2)

@@ -21,14 +21,16 @@ def _torch():
     return torch
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 4])
 @pytest.mark.parametrize("M,N,K,epi", [
     (128, 256, 64, 0), (1000, 768, 768, 0), (777, 2304, 768, 0), (640, 3072, 768, 1),
     (513, 768, 3072, 2), (300, 128, 256, 2), (4096, 1024, 256, 1), (129, 384, 512, 0),
     (100000, 2304, 768, 0), (70000, 768, 3072, 2),
 ])
 def test_tc_gemm_matches_torch(lv, M, N, K, epi, mode):
-    """mode 0: 2-CTA (cta_group::2) kernel where N % 256 == 0; mode 1: 1-CTA kernel."""
+    """mode 0: 2-CTA (cta_group::2) kernel where N % 256 == 0 (long-K residual GEMMs on the
+    1-buffer / 5-stage variant); mode 1: 1-CTA kernel; mode 4: 2-buffer / 4-stage variant for
+    every residual GEMM."""
     torch = _torch()
     from paper_2506_08276_b200 import _lib
     _lib.lib().lv_set_gemm_mode(mode)
