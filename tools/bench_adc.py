@@ -25,25 +25,26 @@ model = PQModel(dim=dim, padded_dim=dim if dim % m == 0 else dim + m - dim % m, 
 codes = PQCodes(codes=rng.integers(0, 256, (n, m), dtype=np.uint8))
 dev = DeviceIndex(g, model, codes)
 lut = torch.randn(m * 256, device="cuda")
-ids = torch.randperm(n, device="cuda")
 out = torch.empty(n, device="cuda")
 st = torch.cuda.current_stream().cuda_stream
 L = _lib.lib()
-for _ in range(3):
-    _lib.check(L.lv_adc_score(dev.handle, lut.data_ptr(), ids.data_ptr(), n, out.data_ptr(),
-                              _lib.LV_IO_DEVICE, st))
-ts = []
-for _ in range(5):
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    _lib.check(L.lv_adc_score(dev.handle, lut.data_ptr(), ids.data_ptr(), n, out.data_ptr(),
-                              _lib.LV_IO_DEVICE, st))
-    e1.record()
-    torch.cuda.synchronize()
-    ts.append(e0.elapsed_time(e1))
-t = sorted(ts)[2]
-gb = n * (m + 12) / 1e9
-print(f"ADC stream: {n} ids x m={m}: {t:.3f} ms, {gb / (t / 1e3):.0f} GB/s algorithmic "
-      f"({n / t / 1e6:.2f} G ids/s)")
+for order in ("random", "sorted"):
+    ids = torch.randperm(n, device="cuda") if order == "random" else torch.arange(n, device="cuda")
+    for _ in range(3):
+        _lib.check(L.lv_adc_score(dev.handle, lut.data_ptr(), ids.data_ptr(), n, out.data_ptr(),
+                                  _lib.LV_IO_DEVICE, st))
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(L.lv_adc_score(dev.handle, lut.data_ptr(), ids.data_ptr(), n, out.data_ptr(),
+                                  _lib.LV_IO_DEVICE, st))
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t = sorted(ts)[2]
+    gb = n * (m + 12) / 1e9
+    print(f"ADC stream ({order} ids): {n} ids x m={m}: {t:.3f} ms, {gb / (t / 1e3):.0f} GB/s "
+          f"algorithmic ({n / t / 1e6:.2f} G ids/s)", flush=True)
 # correctness: tests/test_gpu_search.py checks lv_adc_score bit-for-bit against the
 # reference-produced golden ADC vectors (m = 32 and m = 64)
