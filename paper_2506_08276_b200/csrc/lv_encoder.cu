@@ -272,39 +272,52 @@ __global__ void ln_stats_finalize_kernel(const float2 *__restrict__ parts, int n
 }
 
 // pool_kernel over LN(y): mean_p LN(y_p) = g * mean_p((y_p - mu_p) * rstd_p) + b,
-// then L2 normalisation. One block per sequence.
-__global__ void pool_ln_kernel(const __nv_bfloat16 *__restrict__ y, const float2 *__restrict__ st,
-                               const float *__restrict__ g, const float *__restrict__ b,
-                               float *__restrict__ out, int S, int d) {
-  __shared__ float red[32];
+// then L2 normalisation. One block per sequence; thread t owns columns
+// [8t, 8t + 8) (16-byte loads, d % 8 == 0, d <= 1024), fixed summation order.
+__global__ void __launch_bounds__(128) pool_ln_kernel(const __nv_bfloat16 *__restrict__ y,
+                                                      const float2 *__restrict__ st,
+                                                      const float *__restrict__ g,
+                                                      const float *__restrict__ b,
+                                                      float *__restrict__ out, int S, int d) {
+  __shared__ float red[4];
   __shared__ float2 sst[512];
   const int64_t seq = blockIdx.x;
-  const __nv_bfloat16 *base = y + seq * S * d;
   for (int p = threadIdx.x; p < S; p += blockDim.x) sst[p] = st[seq * S + p];
   __syncthreads();
-  float local = 0.f;
-  float mv[4];
-  int nv = 0;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    float acc = 0.f;
-    for (int p = 0; p < S; ++p)
-      acc = fmaf(__bfloat162float(base[(size_t)p * d + c]) - sst[p].x, sst[p].y, acc);
-    const float v = fmaf(g[c], acc / (float)S, b[c]);
-    mv[nv++] = v;
-    local += v * v;
+  const int c0 = 8 * threadIdx.x;
+  const bool live = c0 < d;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (live) {
+    const uint4 *base = reinterpret_cast<const uint4 *>(y + seq * S * d + c0);
+    const int stride = d / 8;
+    for (int p = 0; p < S; ++p) {
+      const uint4 u = __ldg(base + (size_t)p * stride);
+      const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+      const float mu = sst[p].x, rs = sst[p].y;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        acc[2 * e] = fmaf(f.x - mu, rs, acc[2 * e]);
+        acc[2 * e + 1] = fmaf(f.y - mu, rs, acc[2 * e + 1]);
+      }
+    }
+  }
+  float v[8], local = 0.f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    v[e] = live ? fmaf(g[c0 + e], acc[e] / (float)S, b[c0 + e]) : 0.f;
+    local += v[e] * v[e];
   }
   local = warp_sum(local);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    t = warp_sum(t);
-    if (threadIdx.x == 0) red[0] = t;
+  const float tot = (red[0] + red[1]) + (red[2] + red[3]);
+  const float inv = 1.0f / fmaxf(sqrtf(tot), 1e-12f);
+  if (live) {
+    float4 *o = reinterpret_cast<float4 *>(out + seq * d + c0);
+    o[0] = make_float4(v[0] * inv, v[1] * inv, v[2] * inv, v[3] * inv);
+    o[1] = make_float4(v[4] * inv, v[5] * inv, v[6] * inv, v[7] * inv);
   }
-  __syncthreads();
-  const float inv = 1.0f / fmaxf(sqrtf(red[0]), 1e-12f);
-  nv = 0;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) out[seq * d + c] = mv[nv++] * inv;
 }
 
 // ---- decoder-style encoder (arch 1, Qwen3-shaped, config-4) kernels --------
@@ -840,7 +853,7 @@ int forward_fused(lv_encoder *e, int64_t ns, int S, int M, float *out, cudaStrea
     LV_TRY(finalize_stats(e, e->st2, M, s));
   }
   const EncLayer &Z = e->layers.back();
-  pool_ln_kernel<<<(unsigned)ns, 256, 0, s>>>(x, e->st2, Z.ln2_g, Z.ln2_b, out, S, d);
+  pool_ln_kernel<<<(unsigned)ns, 128, 0, s>>>(x, e->st2, Z.ln2_g, Z.ln2_b, out, S, d);
   note_launch();
   LV_CHECK_CUDA(cudaGetLastError());
   return LV_OK;
