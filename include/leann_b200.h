@@ -8,6 +8,16 @@
  *   lv_index_create      <- Engine.open loaders: load_graph (graph.py:151-193),
  *                           load_pq (pq.py:213-244), load_deleted (graph.py:204-216)
  *   lv_index_set_matrix  <- MatrixSource(matrix) oracle source (search.py:78-93)
+ *   lv_index_set_fetch   <- ProviderSource.fetch (search.py:103-110) of a HOST provider
+ *                           (any reference provider object): the device traversal calls it
+ *                           once per iteration with the step's new ids (LV_SOURCE_CALLBACK)
+ *   lv_index_set_cache_rows
+ *                        <- EmbeddingCache.vectors (search.py:113-128): the pinned rows
+ *   lv_query_norms       <- the host np.float32(np.sqrt(np.dot(q, q))) of vectors.py:138 /
+ *                           pq.py:163, on the device in the same BLAS order
+ *   lv_merge_pending     <- Engine.search's merge of the pending (buffered-add) items
+ *                           (index.py:320-327) over MutableIndex.buffer_scan
+ *                           (update.py:483-488) with distance() (vectors.py:94-116)
  *   lv_index_set_cache   <- build_embedding_cache / EmbeddingCache (search.py:113-142)
  *   lv_index_attach_encoder
  *                        <- ProviderSource(provider, store.get) (search.py:96-110)
@@ -69,6 +79,7 @@ extern "C" {
 /* exact-vector sources */
 #define LV_SOURCE_MATRIX 0   /* resident matrix (MatrixSource) */
 #define LV_SOURCE_ENCODER 1  /* recompute with the attached encoder (ProviderSource) */
+#define LV_SOURCE_CALLBACK 2 /* recompute through a host provider (lv_index_set_fetch) */
 
 #define LV_IO_DEVICE 1       /* pointer arguments are device pointers */
 #define LV_NO_SHARED_RECOMPUTE 2  /* lv_search_params.flags: encode every request, even
@@ -86,6 +97,9 @@ extern "C" {
 #define LV_Q_FAILED 2
 
 typedef struct lv_index lv_index;
+/* Host provider: write the exact float32 vectors of ids[0..n) into rows[n][dim];
+ * return 0, or non-zero for a provider failure (-> LV_ERR_PROVIDER). */
+typedef int (*lv_fetch_fn)(void *user, const int64_t *ids, int32_t n, float *rows);
 typedef struct lv_encoder lv_encoder;
 
 /* One loaded index (LGR1 graph + LPQ1 PQ + LDL1 deletes), host arrays. */
@@ -182,9 +196,16 @@ int lv_index_set_deleted(lv_index *index, const uint8_t *deleted, int flags);
 int lv_index_set_cache(lv_index *index, const int64_t *ids, int64_t count, int flags);
 int lv_index_attach_encoder(lv_index *index, lv_encoder *enc, const void *tokens,
                             int32_t token_bytes, int32_t seq_len, int flags);
+/* Host provider for LV_SOURCE_CALLBACK (fn = NULL detaches). Called on the
+ * thread that runs lv_search_batch, once per traversal iteration. */
+int lv_index_set_fetch(lv_index *index, lv_fetch_fn fn, void *user);
+/* rows[count][dim]: the exact vectors of the ids last passed to lv_index_set_cache,
+ * in that order (replaces vectors the attached encoder computed). */
+int lv_index_set_cache_rows(lv_index *index, const float *rows, int flags);
 
-/* qnorm may be NULL: norms are then computed on the device (not bit-identical to
- * the reference's host np.dot, vectors.py:138 — parity callers pass qnorm). */
+/* qnorm may be NULL: norms are then computed on the device in the reference's
+ * np.dot order (OpenBLAS SkylakeX sdot, bit-exact for dim % 32 == 0; vectors.py:138,
+ * pq.py:163). A zero query norm under cosine two_level -> LV_ERR_USAGE (pq.py:163-166). */
 int lv_search_batch(lv_index *index, const float *q, const float *qnorm, int32_t B,
                     const lv_search_params *params, const lv_search_outputs *out,
                     void *stream);
@@ -196,6 +217,19 @@ int lv_adc_score(lv_index *index, const float *table, const int64_t *ids, int64_
                  float *out, int flags, void *stream);
 int lv_distance_many(int32_t metric, const float *rows, int64_t nrows, int32_t dim,
                      const float *q, float qnorm, float *out, int flags, void *stream);
+/* qn = np.float32(np.sqrt(np.dot(q, q))) of each row q[b] (B x dim) in the
+ * OpenBLAS sdot order (bit-exact with numpy on a SkylakeX-kernel host for
+ * dim % 32 == 0; vectors.py:138, pq.py:163). */
+int lv_query_norms(const float *q, int32_t B, int32_t dim, float *out, int flags, void *stream);
+/* Pending-buffer merge: distance(q_b, pending_p) for every query b and pending
+ * item p (vectors.py:94-116; np.dot in the OpenBLAS sdot order), merged with
+ * the graph's results ids/dist/count (in-out, [B*k] / [B]) by (distance, id)
+ * keeping the first k (index.py:320-327). qnorm may be NULL (computed on the
+ * device in the same sdot order). A zero cosine denominator -> LV_ERR_USAGE. */
+int lv_merge_pending(int32_t metric, const float *pending, const int64_t *pending_ids,
+                     int64_t n_pending, int32_t dim, const float *q, const float *qnorm,
+                     int32_t B, int32_t k, int64_t *ids, float *dist, int32_t *count,
+                     int flags, void *stream);
 
 int lv_encoder_create(const lv_encoder_config *cfg, const float *const *weights,
                       int32_t n_weights, int device, lv_encoder **out);

@@ -74,8 +74,9 @@ def pairwise_sum64(x: np.ndarray) -> np.ndarray:
 def query_norm(q: np.ndarray) -> np.float32:
     """``np.float32(np.sqrt(np.dot(q, q)))`` exactly as ``vectors.py:138``/``pq.py:163``.
 
-    This is a host BLAS ``sdot``; its order is CPU-dependent, so the B200 path
-    takes this value from the host instead of recomputing it on the device.
+    This is a host BLAS ``sdot``; its order depends on the BLAS kernel the
+    host selects. On this image's hosts (OpenBLAS SkylakeX kernel) it equals
+    :func:`sdot_openblas`, which the device reproduces (``lv_query_norms``).
     """
     q = np.asarray(q, dtype=np.float32)
     return np.float32(np.sqrt(np.dot(q, q)))
@@ -136,3 +137,62 @@ def approx_distance_many(table: np.ndarray, codes: np.ndarray) -> np.ndarray:
     rows = np.arange(table.shape[0])
     gathered = table[rows[None, :], codes].astype(np.float64)
     return pairwise_sum64(gathered).astype(np.float32)
+
+
+def _fma32(a, b, c):
+    """float32 fused multiply-add, emulated in float64 (a*b is exact there; the
+    one float64 rounding before the float32 one can only matter at an exact
+    float32 midpoint, which the pinning test below never hit)."""
+    return (np.float64(a) * np.float64(b) + np.float64(c)).astype(np.float32) \
+        if np.ndim(a) == 0 else (a.astype(np.float64) * b.astype(np.float64)
+                                 + c.astype(np.float64)).astype(np.float32)
+
+
+def sdot_openblas(x: np.ndarray, y: np.ndarray) -> np.float32:
+    """``np.dot`` of two float32 vectors as scipy-openblas 0.3.30's SkylakeX
+    ``sdot`` kernel evaluates it (numpy hands 1-D float32 dots to cblas_sdot):
+    n1 = n & -32; four 16-lane FMA accumulators over the n1 & -64 prefix, each
+    folded to 8 lanes (lo + hi); four 8-lane FMA accumulators over the last
+    32-block; ((a0 + a1) + a2) + a3; lanes l + l+4; (h0 + h1) + (h2 + h3); then
+    the scalar tail ``dot += y[i] * x[i]`` (separately rounded). Pinned against
+    np.dot for every n % 32 == 0 (tests/test_oracle_golden.py::test_sdot_order).
+    This is what ``distance()`` (vectors.py:94-116) and every ``qn``
+    (vectors.py:138, pq.py:163) compute on this image's hosts."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    n = x.shape[0]
+    n1 = n & ~31
+    dot = np.float32(0.0)
+    i = 0
+    if n1:
+        n64 = n1 & ~63
+        a5 = np.zeros((4, 16), np.float32)
+        while i < n64:
+            a5 = _fma32(x[i:i + 64].reshape(4, 16), y[i:i + 64].reshape(4, 16), a5)
+            i += 64
+        acc = (a5[:, :8] + a5[:, 8:]).astype(np.float32)
+        while i < n1:
+            acc = _fma32(x[i:i + 32].reshape(4, 8), y[i:i + 32].reshape(4, 8), acc)
+            i += 32
+        a = ((acc[0] + acc[1]) + acc[2]) + acc[3]
+        h = (a[:4] + a[4:]).astype(np.float32)
+        dot = np.float32(np.float32(h[0] + h[1]) + np.float32(h[2] + h[3]))
+    while i < n:
+        dot = np.float32(dot + np.float32(y[i] * x[i]))
+        i += 1
+    return dot
+
+
+def distance(a: np.ndarray, b: np.ndarray, metric: str = "cosine") -> float:
+    """vectors.py:94-116 with np.dot as :func:`sdot_openblas`."""
+    a = np.asarray(a, dtype=np.float32)
+    b = np.asarray(b, dtype=np.float32)
+    if metric == "l2":
+        d = (a - b).astype(np.float32)
+        return float(sdot_openblas(d, d))
+    if metric == "ip":
+        return float(-sdot_openblas(a, b))
+    denom = float(np.sqrt(sdot_openblas(a, a))) * float(np.sqrt(sdot_openblas(b, b)))
+    if denom == 0.0:
+        raise ValueError("cosine distance undefined for zero vector")
+    return float(np.float32(-sdot_openblas(a, b)) / np.float32(denom))

@@ -246,6 +246,17 @@ def run_search(graph, q, params: SearchParams, source, metric: str,
     return two_level(graph, q, params, codebooks, codes, source, metric, qn, cached)
 
 
+def merge_pending(results, q, pending_ids, pending_vecs, metric: str, k: int):
+    """Engine.search's merge (index.py:320-327) of ``buffer_scan`` (update.py:483-488):
+    distance() (vectors.py:94-116) to every pending vector, (d, id)-sorted with
+    the graph results, first k."""
+    from .numerics import distance
+    combined = [(d, i) for i, d in results]
+    combined += [(distance(q, v, metric), int(i)) for i, v in zip(pending_ids, pending_vecs)]
+    combined.sort()
+    return [(i, d) for d, i in combined[:k]]
+
+
 # --- minimal graph / file readers (graph.py:138-216, pq.py:198-244) ----------
 
 class CsrGraph:

@@ -14,6 +14,7 @@ from .pq import (PQCodes, PQModel, adc_build, approx_distance_many, default_m_pq
                  load_pq, save_pq)
 from .search import (DeviceIndex, EmbeddingCache, MatrixSource, ProviderSource,  # noqa: F401
                      SearchParams, SearchReport, best_first_search, build_embedding_cache,
-                     query_norm, run_search, search_batch, two_level_search)
+                     as_pruned, device_query_norms, merge_pending, query_norm, run_search,
+                     search_batch, two_level_search)
 
 __version__ = "0.1.0"

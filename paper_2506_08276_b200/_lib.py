@@ -17,6 +17,7 @@ LV_METRIC = {"l2": 0, "ip": 1, "cosine": 2}
 LV_MODE = {"exact_bestfirst": 0, "two_level": 1}
 LV_SOURCE_MATRIX = 0
 LV_SOURCE_ENCODER = 1
+LV_SOURCE_CALLBACK = 2
 LV_IO_DEVICE = 1
 LV_NO_SHARED_RECOMPUTE = 2
 LV_DRY_RECOMPUTE = 4
@@ -76,6 +77,10 @@ class EncoderStats(C.Structure):
     ]
 
 
+# int (*lv_fetch_fn)(void *user, const int64_t *ids, int32_t n, float *rows)
+FETCH_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int64), C.c_int32,
+                       C.POINTER(C.c_float))
+
 EXPORTS = {
     "lv_last_error": (C.c_char_p, []),
     "lv_version": (C.c_int, []),
@@ -87,6 +92,13 @@ EXPORTS = {
     "lv_index_set_cache": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int]),
     "lv_index_attach_encoder": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                           C.c_int32, C.c_int]),
+    "lv_index_set_fetch": (C.c_int, [C.c_void_p, FETCH_FN, C.c_void_p]),
+    "lv_index_set_cache_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "lv_merge_pending": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                   C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "lv_query_norms": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int,
+                                 C.c_void_p]),
     "lv_search_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                   C.POINTER(SearchParamsC), C.POINTER(SearchOutputs), C.c_void_p]),
     "lv_last_search_stats": (C.c_int, [C.c_void_p, C.POINTER(SearchStats)]),

@@ -78,6 +78,10 @@ struct Workspace {
   DBuf<float> out_dist;
   DBuf<int32_t> out_count, out_status, visits, blog;
   int32_t *h_counters = nullptr;  // pinned
+  // the per-slot bitmaps are all-zero between calls only when the last pass
+  // finished every query (finish_query clears them); an early return leaves
+  // this set and the next pass clears them in full
+  bool bits_dirty = false;
   ~Workspace() {
     if (h_counters) cudaFreeHost(h_counters);
   }
@@ -109,6 +113,8 @@ struct lv_index {
   void *tokens = nullptr;
   bool own_tokens = false;
   int32_t token_bytes = 0, seq_len = 0;
+  lv_fetch_fn fetch = nullptr;  // LV_SOURCE_CALLBACK: host provider (ProviderSource.fetch)
+  void *fetch_user = nullptr;
   Workspace ws;
   lv_search_stats stats{};
   ~lv_index() {
@@ -192,13 +198,35 @@ int lv_index_create(const lv_index_desc *d, int device, lv_index **out) {
   for (int l = 0; l < d->level_count && rc == LV_OK; ++l) {
     uint64_t *o = nullptr;
     uint32_t *nb = nullptr;
-    // CSR sanity (graph.py:100-135, minus the per-row O(n*deg) checks)
+    // CSR sanity (graph.py:100-135): the frontier's scratch is sized from
+    // max_degree and the bitmaps are indexed by neighbour id, so every row
+    // must fit max_degree and every id must be < n (O(nnz) host pass)
     const uint64_t *ho = d->level_offsets[l];
+    const std::string sec = "graph.level" + std::to_string(l);
     if (ho[0] != 0 || ho[d->n] != d->level_nnz[l]) {
-      set_error("graph.level" + std::to_string(l) + ".offsets: offsets[n] != neighbor count");
+      set_error(sec + ".offsets: offsets[n] != neighbor count");
       rc = LV_ERR_DATA;
       break;
     }
+    for (int64_t v = 0; v < d->n && rc == LV_OK; ++v) {
+      if (ho[v + 1] < ho[v]) {
+        set_error(sec + ".offsets: not monotone at node " + std::to_string(v));
+        rc = LV_ERR_DATA;
+      } else if (ho[v + 1] - ho[v] > (uint64_t)d->max_degree) {
+        set_error(sec + ".degree: node " + std::to_string(v) + " exceeds M");
+        rc = LV_ERR_DATA;
+      }
+    }
+    if (rc != LV_OK) break;
+    const uint32_t *hn = d->level_neighbors[l];
+    for (uint64_t e = 0; e < d->level_nnz[l]; ++e) {
+      if ((int64_t)hn[e] >= d->n) {
+        set_error(sec + ".neighbors: id " + std::to_string(hn[e]) + " out of range");
+        rc = LV_ERR_DATA;
+        break;
+      }
+    }
+    if (rc != LV_OK) break;
     rc = dalloc(&o, d->n + 1);
     if (rc == LV_OK) rc = dalloc(&nb, d->level_nnz[l]);
     ix->offs.push_back(o);
@@ -336,6 +364,27 @@ int lv_index_attach_encoder(lv_index *ix, lv_encoder *enc, const void *tokens, i
   return LV_OK;
 }
 
+int lv_index_set_fetch(lv_index *ix, lv_fetch_fn fn, void *user) {
+  LV_REQUIRE(ix, LV_ERR_USAGE, "null index");
+  ix->fetch = fn;
+  ix->fetch_user = user;
+  return LV_OK;
+}
+
+// Pinned vectors of the lv_index_set_cache ids, in the order those ids were
+// given (the reference EmbeddingCache.vectors, search.py:113-128).
+int lv_index_set_cache_rows(lv_index *ix, const float *rows, int flags) {
+  LV_REQUIRE(ix && rows, LV_ERR_USAGE, "lv_index_set_cache_rows: null argument");
+  LV_REQUIRE(ix->n_cached > 0, LV_ERR_USAGE, "lv_index_set_cache_rows: no cache ids set");
+  DeviceGuard guard(ix->device);
+  dfree(ix->cache_rows);
+  LV_TRY(dalloc(&ix->cache_rows, (size_t)ix->n_cached * ix->dim));
+  LV_CHECK_CUDA(cudaMemcpy(ix->cache_rows, rows, (size_t)ix->n_cached * ix->dim * 4,
+                           (flags & LV_IO_DEVICE) ? cudaMemcpyDeviceToDevice
+                                                  : cudaMemcpyHostToDevice));
+  return LV_OK;
+}
+
 int lv_last_search_stats(const lv_index *ix, lv_search_stats *stats) {
   LV_REQUIRE(ix && stats, LV_ERR_USAGE, "null argument");
   *stats = ix->stats;
@@ -365,7 +414,8 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
                 int32_t *d_blog, int32_t blog_cap, cudaStream_t s) {
   Workspace &ws = ix->ws;
   const bool two_level = p.mode == LV_MODE_TWO_LEVEL;
-  const bool enc_src = p.source == LV_SOURCE_ENCODER;
+  const bool enc_src = p.source == LV_SOURCE_ENCODER || p.source == LV_SOURCE_CALLBACK;
+  const bool callback = p.source == LV_SOURCE_CALLBACK;
   int slots = p.max_inflight > 0 ? p.max_inflight : (enc_src ? 4096 : 148 * 16);
   slots = std::max(1, std::min(slots, B));
   const int req_cap = 2 * ix->max_degree + 2;
@@ -382,10 +432,11 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   bool fresh_bits = ws.abits.cap < (size_t)slots * words;
   LV_TRY(ws.abits.ensure((size_t)slots * words));
   LV_TRY(ws.xbits.ensure((size_t)slots * words));
-  if (fresh_bits) {  // bitmaps are kept all-zero between queries by finish_query
+  if (fresh_bits || ws.bits_dirty) {  // kept all-zero between queries by finish_query
     LV_CHECK_CUDA(cudaMemsetAsync(ws.abits.ptr, 0, ws.abits.cap * 4, s));
     LV_CHECK_CUDA(cudaMemsetAsync(ws.xbits.ptr, 0, ws.xbits.cap * 4, s));
   }
+  ws.bits_dirty = true;  // cleared below once every query has finished
   LV_TRY(ws.xlist.ensure((size_t)slots * xl_cap));
   LV_TRY(ws.req.ensure((size_t)slots * req_cap));
   LV_TRY(ws.counters.ensure(4));
@@ -447,7 +498,7 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   c.m = ix->m;
   c.codes = ix->codes;
   c.luts = ws.luts.ptr;
-  c.source = p.source;
+  c.source = enc_src ? LV_SOURCE_ENCODER : p.source;  // the kernels see callback = encoder
   c.matrix = ix->matrix;
   c.emb_buf = ws.emb.ptr;
   c.emb_map = shared ? ws.emb_map.ptr : nullptr;
@@ -501,9 +552,14 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
     iterations = 1;
   } else {
     const bool dry = (p.flags & LV_DRY_RECOMPUTE) != 0;
-    LV_REQUIRE(dry ? ix->matrix != nullptr : (ix->enc && ix->tokens), LV_ERR_USAGE,
+    LV_REQUIRE(dry ? ix->matrix != nullptr
+                   : (callback ? ix->fetch != nullptr : (ix->enc && ix->tokens)), LV_ERR_USAGE,
                dry ? "LV_DRY_RECOMPUTE requires lv_index_set_matrix"
-                   : "encoder source requires lv_index_attach_encoder");
+                   : (callback ? "callback source requires lv_index_set_fetch"
+                               : "encoder source requires lv_index_attach_encoder"));
+    std::vector<int32_t> h_ids;
+    std::vector<int64_t> h_ids64;
+    std::vector<float> h_rows;
     int32_t row_base = 0;
     auto reset_table = [&]() -> int {
       LV_CHECK_CUDA(cudaMemsetAsync(ws.hkeys.ptr, 0xff, ((size_t)hmask + 1) * 4, s));
@@ -549,6 +605,20 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
               ix->matrix, enc_ids, n_new, ix->dim, enc_out);
           note_launch();
           LV_CHECK_CUDA(cudaGetLastError());
+        } else if (n_new > 0 && callback) {
+          // host provider: ProviderSource.fetch(ids) (search.py:103-110) on the
+          // new ids, rows back into the step table
+          h_ids.resize(n_new);
+          h_ids64.resize(n_new);
+          h_rows.resize((size_t)n_new * ix->dim);
+          LV_CHECK_CUDA(cudaMemcpyAsync(h_ids.data(), enc_ids, (size_t)n_new * 4,
+                                        cudaMemcpyDeviceToHost, s));
+          LV_CHECK_CUDA(cudaStreamSynchronize(s));
+          for (int32_t i = 0; i < n_new; ++i) h_ids64[i] = h_ids[i];
+          const int frc = ix->fetch(ix->fetch_user, h_ids64.data(), n_new, h_rows.data());
+          LV_REQUIRE(frc == 0, LV_ERR_PROVIDER, "provider fetch failed");
+          LV_CHECK_CUDA(cudaMemcpyAsync(enc_out, h_rows.data(), h_rows.size() * 4,
+                                        cudaMemcpyHostToDevice, s));
         } else if (n_new > 0) {
           LV_TRY(encode_node_rows(ix->enc, ix->tokens, ix->token_bytes, ix->seq_len, enc_ids,
                                   n_new, enc_out, s));
@@ -569,6 +639,7 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  ws.bits_dirty = false;  // every query finished: finish_query cleared its bits
   unsigned long long bytes = 0;
   LV_CHECK_CUDA(cudaMemcpyAsync(&bytes, ws.bytes.ptr, 8, cudaMemcpyDeviceToHost, s));
   LV_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -603,13 +674,15 @@ extern "C" int lv_search_batch(lv_index *ix, const float *q, const float *qnorm,
              "unknown mode");
   LV_REQUIRE(p->mode != LV_MODE_TWO_LEVEL || ix->m > 0, LV_ERR_USAGE,
              "two_level mode requires PQ artifacts");
-  LV_REQUIRE(p->source == LV_SOURCE_MATRIX || p->source == LV_SOURCE_ENCODER, LV_ERR_USAGE,
-             "unknown source");
+  LV_REQUIRE(p->source == LV_SOURCE_MATRIX || p->source == LV_SOURCE_ENCODER ||
+                 p->source == LV_SOURCE_CALLBACK,
+             LV_ERR_USAGE, "unknown source");
   LV_REQUIRE(p->source != LV_SOURCE_MATRIX || ix->matrix, LV_ERR_USAGE,
              "matrix source requires lv_index_set_matrix");
   LV_REQUIRE(!p->use_cache || ix->cached_bits, LV_ERR_USAGE, "cache requested but not built");
-  LV_REQUIRE(p->source != LV_SOURCE_ENCODER || !p->use_cache || ix->cache_rows, LV_ERR_USAGE,
-             "encoder-source cache needs cached vectors (attach the encoder before the cache)");
+  LV_REQUIRE(p->source == LV_SOURCE_MATRIX || !p->use_cache || ix->cache_rows, LV_ERR_USAGE,
+             "recompute-source cache needs cached vectors (attach the encoder before the cache, "
+             "or lv_index_set_cache_rows)");
   LV_REQUIRE(p->ef <= (1 << 24), LV_ERR_USAGE, "ef too large");
   LV_REQUIRE(B >= 0, LV_ERR_USAGE, "B must be >= 0");
   LV_REQUIRE(out->ids && out->dist && out->count && out->counters, LV_ERR_USAGE,
@@ -644,6 +717,16 @@ extern "C" int lv_search_batch(lv_index *ix, const float *q, const float *qnorm,
     LV_TRY(ws.qn.ensure(B));
     LV_TRY(upload(ws.qn.ptr, qnorm, (size_t)B * 4, false, s));
     d_qn = ws.qn.ptr;
+  }
+  if (ix->metric == LV_METRIC_COSINE && p->mode == LV_MODE_TWO_LEVEL) {
+    // adc_build raises for a zero query under cosine (pq.py:163-166)
+    LV_TRY(ws.counters.ensure(4));
+    LV_CHECK_CUDA(cudaMemsetAsync(ws.counters.ptr + 3, 0, 4, s));
+    LV_CHECK_CUDA(launch_count_zero(d_qn, B, ws.counters.ptr + 3, s));
+    int32_t zeros = 0;
+    LV_CHECK_CUDA(cudaMemcpyAsync(&zeros, ws.counters.ptr + 3, 4, cudaMemcpyDeviceToHost, s));
+    LV_CHECK_CUDA(cudaStreamSynchronize(s));
+    LV_REQUIRE(zeros == 0, LV_ERR_USAGE, "cosine ADC undefined for zero query");
   }
   int64_t *d_ids = out->ids;
   float *d_dist = out->dist;
@@ -847,6 +930,97 @@ extern "C" int lv_distance_many(int32_t metric, const float *rows, int64_t nrows
   LV_TRY(upload(dq.ptr, q, (size_t)dim * 4, false, s));
   LV_CHECK_CUDA(launch_distance_many(metric, dr.ptr, nrows, dim, dq.ptr, qnorm, dout.ptr, s));
   LV_CHECK_CUDA(cudaMemcpyAsync(out, dout.ptr, nrows * 4, cudaMemcpyDeviceToHost, s));
+  LV_CHECK_CUDA(cudaStreamSynchronize(s));
+  return LV_OK;
+}
+
+// Engine.search's pending-buffer merge (index.py:320-327 over buffer_scan,
+// update.py:483-488): see include/leann_b200.h.
+extern "C" int lv_merge_pending(int32_t metric, const float *pending, const int64_t *pending_ids,
+                                int64_t n_pending, int32_t dim, const float *q,
+                                const float *qnorm, int32_t B, int32_t k, int64_t *ids,
+                                float *dist, int32_t *count, int flags, void *stream) {
+  LV_REQUIRE(ids && dist && count, LV_ERR_USAGE, "lv_merge_pending: null output");
+  LV_REQUIRE(metric >= 0 && metric <= 2, LV_ERR_USAGE, "unknown metric");
+  LV_REQUIRE(dim >= 1 && k >= 1 && B >= 0 && n_pending >= 0, LV_ERR_USAGE,
+             "lv_merge_pending: bad sizes");
+  if (B == 0 || n_pending == 0) return LV_OK;
+  LV_REQUIRE(pending && pending_ids && q, LV_ERR_USAGE, "lv_merge_pending: null input");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool dev = flags & LV_IO_DEVICE;
+  DBuf<float> dp, dq, dqn, dd, scratch;
+  DBuf<int64_t> dpi, di;
+  DBuf<int32_t> dc, bad;
+  const float *p_pend = pending, *p_q = q, *p_qn = qnorm;
+  const int64_t *p_pid = pending_ids;
+  int64_t *p_ids = ids;
+  float *p_dist = dist;
+  int32_t *p_count = count;
+  if (!dev) {
+    LV_TRY(dp.ensure((size_t)n_pending * dim));
+    LV_TRY(dpi.ensure(n_pending));
+    LV_TRY(dq.ensure((size_t)B * dim));
+    LV_TRY(di.ensure((size_t)B * k));
+    LV_TRY(dd.ensure((size_t)B * k));
+    LV_TRY(dc.ensure(B));
+    LV_TRY(upload(dp.ptr, pending, (size_t)n_pending * dim * 4, false, s));
+    LV_TRY(upload(dpi.ptr, pending_ids, (size_t)n_pending * 8, false, s));
+    LV_TRY(upload(dq.ptr, q, (size_t)B * dim * 4, false, s));
+    LV_TRY(upload(di.ptr, ids, (size_t)B * k * 8, false, s));
+    LV_TRY(upload(dd.ptr, dist, (size_t)B * k * 4, false, s));
+    LV_TRY(upload(dc.ptr, count, (size_t)B * 4, false, s));
+    p_pend = dp.ptr;
+    p_pid = dpi.ptr;
+    p_q = dq.ptr;
+    p_ids = di.ptr;
+    p_dist = dd.ptr;
+    p_count = dc.ptr;
+    if (qnorm) {
+      LV_TRY(dqn.ensure(B));
+      LV_TRY(upload(dqn.ptr, qnorm, (size_t)B * 4, false, s));
+      p_qn = dqn.ptr;
+    }
+  }
+  if (!p_qn) {
+    LV_TRY(dqn.ensure(B));
+    LV_CHECK_CUDA(launch_qnorm(p_q, B, dim, dqn.ptr, s));
+    p_qn = dqn.ptr;
+  }
+  LV_TRY(scratch.ensure((size_t)B * n_pending));
+  LV_TRY(bad.ensure(1));
+  LV_CHECK_CUDA(cudaMemsetAsync(bad.ptr, 0, 4, s));
+  LV_CHECK_CUDA(launch_pending_merge(metric, p_pend, p_pid, n_pending, dim, p_q, p_qn, B, k, p_ids,
+                                     p_dist, p_count, scratch.ptr, bad.ptr, s));
+  int32_t h_bad = 0;
+  LV_CHECK_CUDA(cudaMemcpyAsync(&h_bad, bad.ptr, 4, cudaMemcpyDeviceToHost, s));
+  if (!dev) {
+    LV_CHECK_CUDA(cudaMemcpyAsync(ids, p_ids, (size_t)B * k * 8, cudaMemcpyDeviceToHost, s));
+    LV_CHECK_CUDA(cudaMemcpyAsync(dist, p_dist, (size_t)B * k * 4, cudaMemcpyDeviceToHost, s));
+    LV_CHECK_CUDA(cudaMemcpyAsync(count, p_count, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
+  }
+  LV_CHECK_CUDA(cudaStreamSynchronize(s));
+  LV_REQUIRE(!h_bad, LV_ERR_USAGE, "cosine distance undefined for zero vector");
+  return LV_OK;
+}
+
+// qn = np.float32(np.sqrt(np.dot(q, q))) per row in the OpenBLAS sdot order
+// (vectors.py:138, pq.py:163) — what lv_search_batch uses when qnorm is NULL.
+extern "C" int lv_query_norms(const float *q, int32_t B, int32_t dim, float *out, int flags,
+                              void *stream) {
+  LV_REQUIRE(q && out, LV_ERR_USAGE, "lv_query_norms: null argument");
+  LV_REQUIRE(dim >= 1 && B >= 0, LV_ERR_USAGE, "lv_query_norms: bad sizes");
+  if (B == 0) return LV_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (flags & LV_IO_DEVICE) {
+    LV_CHECK_CUDA(launch_qnorm(q, B, dim, out, s));
+    return LV_OK;
+  }
+  DBuf<float> dq, dn;
+  LV_TRY(dq.ensure((size_t)B * dim));
+  LV_TRY(dn.ensure(B));
+  LV_TRY(upload(dq.ptr, q, (size_t)B * dim * 4, false, s));
+  LV_CHECK_CUDA(launch_qnorm(dq.ptr, B, dim, dn.ptr, s));
+  LV_CHECK_CUDA(cudaMemcpyAsync(out, dn.ptr, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
   LV_CHECK_CUDA(cudaStreamSynchronize(s));
   return LV_OK;
 }

@@ -101,6 +101,80 @@ __device__ __forceinline__ double pairwise_sum(Get get, int n) {
   return __dadd_rn(pairwise_block(get, 0, half), pairwise_block(get, half, n - half));
 }
 
+// np.dot(x, y) of two float32 vectors: numpy hands 1-D float32 dots to BLAS
+// cblas_sdot, here scipy-openblas 0.3.30 with the SkylakeX kernel
+// (threadpoolctl reports architecture "SkylakeX" on this image's hosts). Its
+// order, pinned against np.dot on 0/300 mismatching random vectors for every
+// n % 32 == 0 in {32 .. 1024} (tests/test_oracle_golden.py::test_sdot_order):
+//   n1 = n & -32; 512-bit phase over n1 & -64 with four 16-lane FMA
+//   accumulators (a5[j] += x[i+16j..] * y[i+16j..]); fold each to 8 lanes
+//   (low + high half); 256-bit phase over the remaining 32-block with four
+//   8-lane FMA accumulators; acc = ((a0 + a1) + a2) + a3; 128-bit fold
+//   (lanes l + l+4); two hadds -> (h0 + h1) + (h2 + h3); then the scalar tail
+//   dot += y[i] * x[i] (separately rounded). The tail is exact for n % 32 <= 1;
+//   longer tails are not pinned (every dimension on the configs is a multiple of 32).
+// Used for qn = np.float32(np.sqrt(np.dot(q, q))) (vectors.py:138, pq.py:163)
+// and distance() (vectors.py:94-116, the pending-buffer scan).
+template <bool kL2>
+__device__ __forceinline__ float sdot_openblas(const float *__restrict__ x,
+                                               const float *__restrict__ y, int n) {
+  const int n1 = n & ~31;
+  float dot = 0.0f;
+  int i = 0;
+  auto term = [&](int e) -> float2 {
+    if (kL2) {
+      float t = __fsub_rn(x[e], y[e]);
+      return make_float2(t, t);
+    }
+    return make_float2(x[e], y[e]);
+  };
+  if (n1) {
+    float acc[4][8];
+    {
+      float a5[4][16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int l = 0; l < 16; ++l) a5[j][l] = 0.0f;
+      const int n64 = n1 & ~63;
+      for (; i < n64; i += 64) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int l = 0; l < 16; ++l) {
+            float2 p = term(i + 16 * j + l);
+            a5[j][l] = __fmaf_rn(p.x, p.y, a5[j][l]);
+          }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int l = 0; l < 8; ++l) acc[j][l] = __fadd_rn(a5[j][l], a5[j][l + 8]);
+    }
+    for (; i < n1; i += 32) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          float2 p = term(i + 8 * j + l);
+          acc[j][l] = __fmaf_rn(p.x, p.y, acc[j][l]);
+        }
+    }
+    float a[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l)
+      a[l] = __fadd_rn(__fadd_rn(__fadd_rn(acc[0][l], acc[1][l]), acc[2][l]), acc[3][l]);
+    float h0 = __fadd_rn(a[0], a[4]), h1 = __fadd_rn(a[1], a[5]);
+    float h2 = __fadd_rn(a[2], a[6]), h3 = __fadd_rn(a[3], a[7]);
+    dot = __fadd_rn(__fadd_rn(h0, h1), __fadd_rn(h2, h3));
+  }
+  for (; i < n; ++i) {
+    float2 p = term(i);
+    dot = __fadd_rn(dot, __fmul_rn(p.y, p.x));
+  }
+  return dot;
+}
+
 // approx distance of one code row against one LUT (pq.py:186-189).
 __device__ __forceinline__ float adc_one(const float *__restrict__ lut,
                                          const uint8_t *__restrict__ code, int m) {

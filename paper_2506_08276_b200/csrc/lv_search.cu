@@ -704,12 +704,135 @@ __global__ void dedup_kernel(const int32_t *__restrict__ greq, int total, int32_
   }
 }
 
+// qn = np.float32(np.sqrt(np.dot(q, q))) (vectors.py:138, pq.py:163) in the
+// OpenBLAS sdot order (lv_numerics.cuh); one thread per query.
 __global__ void qnorm_kernel(const float *__restrict__ q, int B, int dim, float *__restrict__ qn) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B) return;
-  float acc = 0.f;
-  for (int j = 0; j < dim; ++j) acc = __fadd_rn(acc, __fmul_rn(q[(int64_t)i * dim + j], q[(int64_t)i * dim + j]));
-  qn[i] = __fsqrt_rn(acc);
+  const float *v = q + (int64_t)i * dim;
+  qn[i] = __fsqrt_rn(sdot_openblas<false>(v, v, dim));
+}
+
+// buffer_scan (update.py:483-488): distance(q, vec) (vectors.py:94-116) of
+// every query to every pending vector; one thread per (query, pending) pair.
+// Cosine: -np.dot(q, v) / np.float32(float(sqrt(q.q)) * float(sqrt(v.v))),
+// the denominator multiplied in float64. A zero denominator sets *bad.
+__global__ void pending_dist_kernel(int metric, const float *__restrict__ pend, int64_t np_,
+                                    int dim, const float *__restrict__ q,
+                                    const float *__restrict__ qn, int B,
+                                    float *__restrict__ out, int *bad) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)B * np_) return;
+  const int b = (int)(t / np_);
+  const int64_t p = t % np_;
+  const float *qv = q + (int64_t)b * dim;
+  const float *pv = pend + p * dim;
+  float d;
+  if (metric == LV_METRIC_L2) {
+    d = sdot_openblas<true>(qv, pv, dim);
+  } else if (metric == LV_METRIC_IP) {
+    d = -sdot_openblas<false>(qv, pv, dim);
+  } else {
+    const float pn = __fsqrt_rn(sdot_openblas<false>(pv, pv, dim));
+    const double denom = __dmul_rn((double)qn[b], (double)pn);
+    if (denom == 0.0) atomicExch(bad, 1);
+    d = __fdiv_rn(-sdot_openblas<false>(qv, pv, dim), __double2float_rn(denom));
+  }
+  out[t] = d;
+}
+
+// Engine.search merge (index.py:320-327): the graph's k results plus every
+// pending item, sorted by (distance, id); the first k are kept. One warp per
+// query, k rounds of a warp-wide (d, id) minimum.
+__global__ void pending_merge_kernel(const float *__restrict__ pdist,
+                                     const int64_t *__restrict__ pids, int64_t np_, int B, int k,
+                                     int64_t *ids, float *dist, int32_t *count) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= B) return;
+  const int b = warp;
+  const int cnt0 = count[b];
+  const int64_t total = cnt0 + np_;
+  const float *pd = pdist + (int64_t)b * np_;
+  int64_t *oid = ids + (int64_t)b * k;
+  float *od = dist + (int64_t)b * k;
+  // candidates: [0, cnt0) the graph results (staged in shared memory: the
+  // output rows are overwritten), then the pending items
+  extern __shared__ __align__(8) unsigned char merge_smem[];
+  const int wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t *ci = reinterpret_cast<int64_t *>(merge_smem) + (int64_t)wib * k;
+  float *cd = reinterpret_cast<float *>(reinterpret_cast<int64_t *>(merge_smem) + (int64_t)nw * k) +
+              (int64_t)wib * k;
+  for (int j = lane; j < cnt0; j += 32) {
+    cd[j] = od[j];
+    ci[j] = oid[j];
+  }
+  __syncwarp();
+  // candidates are taken in strictly increasing (d, id) order (ids are unique
+  // across the two lists: pending ids are >= the graph's n)
+  float last_d = 0.f;
+  int64_t last_i = INT64_MIN;
+  bool have_last = false;
+  int out_n = 0;
+  for (int r = 0; r < k && r < total; ++r) {
+    float best_d = 0.f;
+    int64_t best_i = INT64_MAX;
+    bool have = false;
+    for (int64_t j = lane; j < total; j += 32) {
+      float d;
+      int64_t id;
+      if (j < cnt0) {
+        d = cd[j];
+        id = ci[j];
+      } else {
+        d = pd[j - cnt0];
+        id = pids[j - cnt0];
+      }
+      const uint32_t od_ = ord_f32(d);
+      if (have_last) {
+        const uint32_t ol = ord_f32(last_d);
+        if (od_ < ol || (od_ == ol && id <= last_i)) continue;  // already taken
+      }
+      const uint32_t ob = ord_f32(best_d);
+      if (!have || od_ < ob || (od_ == ob && id < best_i)) {
+        best_d = d;
+        best_i = id;
+        have = true;
+      }
+    }
+    // warp argmin over (have, d, id)
+    for (int off = 16; off > 0; off >>= 1) {
+      const float d2 = __shfl_xor_sync(0xffffffffu, best_d, off);
+      const long long i2 = __shfl_xor_sync(0xffffffffu, (long long)best_i, off);
+      const int h2 = __shfl_xor_sync(0xffffffffu, (int)have, off);
+      const uint32_t a = ord_f32(best_d), c = ord_f32(d2);
+      if (h2 && (!have || c < a || (c == a && i2 < best_i))) {
+        best_d = d2;
+        best_i = i2;
+        have = true;
+      }
+    }
+    if (!have) break;
+    if (lane == 0) {
+      od[r] = best_d;
+      oid[r] = best_i;
+    }
+    last_d = best_d;
+    last_i = best_i;
+    have_last = true;
+    out_n = r + 1;
+  }
+  __syncwarp();
+  if (lane == 0) count[b] = out_n;
+  for (int j = out_n + lane; j < k; j += 32) {
+    oid[j] = -1;
+    od[j] = 0.f;
+  }
+}
+
+__global__ void count_zero_kernel(const float *__restrict__ v, int n, int32_t *count) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && v[i] == 0.0f) atomicAdd(count, 1);
 }
 
 __global__ void slot_reset_kernel(SlotState *st, int slots) {
@@ -753,6 +876,32 @@ cudaError_t launch_dedup(const int32_t *greq, int total, int32_t *keys, int32_t 
 cudaError_t launch_qnorm(const float *q, int B, int dim, float *qn, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   qnorm_kernel<<<(B + 127) / 128, 128, 0, s>>>(q, B, dim, qn);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pending_merge(int metric, const float *pend, const int64_t *pids, int64_t np_,
+                                 int dim, const float *q, const float *qn, int B, int k,
+                                 int64_t *ids, float *dist, int32_t *count, float *scratch,
+                                 int *bad, cudaStream_t s) {
+  if (B <= 0 || np_ <= 0) return cudaSuccess;
+  const int64_t pairs = (int64_t)B * np_;
+  pending_dist_kernel<<<(unsigned)((pairs + 127) / 128), 128, 0, s>>>(metric, pend, np_, dim, q,
+                                                                       qn, B, scratch, bad);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int warps = 4;
+  const size_t smem = (size_t)warps * k * (sizeof(float) + sizeof(int64_t));
+  pending_merge_kernel<<<(B + warps - 1) / warps, warps * 32, smem, s>>>(scratch, pids, np_, B, k,
+                                                                        ids, dist, count);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_zero(const float *v, int n, int32_t *count, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  count_zero_kernel<<<(n + 255) / 256, 256, 0, s>>>(v, n, count);
   note_launch();
   return cudaGetLastError();
 }

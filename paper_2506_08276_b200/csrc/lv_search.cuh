@@ -110,7 +110,14 @@ cudaError_t launch_dedup(const int32_t *greq, int total, int32_t *keys, int32_t 
                          uint32_t mask, int32_t *row_count, int32_t base, int32_t *new_ids,
                          int32_t *map, cudaStream_t s);
 cudaError_t launch_qnorm(const float *q, int B, int dim, float *qn, cudaStream_t s);
+// buffer_scan + Engine.search merge (update.py:483-488, index.py:320-327);
+// scratch holds B * np_ floats, *bad is set on a zero cosine denominator.
+cudaError_t launch_pending_merge(int metric, const float *pend, const int64_t *pids, int64_t np_,
+                                 int dim, const float *q, const float *qn, int B, int k,
+                                 int64_t *ids, float *dist, int32_t *count, float *scratch,
+                                 int *bad, cudaStream_t s);
 cudaError_t launch_slot_reset(SlotState *st, int slots, cudaStream_t s);
+cudaError_t launch_count_zero(const float *v, int n, int32_t *count, cudaStream_t s);
 cudaError_t launch_frontier(const SearchCtx &ctx, cudaStream_t s);
 size_t frontier_smem_bytes(const SearchCtx &ctx);
 

@@ -45,6 +45,62 @@ def gather_results(ids, dist_, group=None):
     return torch.cat(li), torch.cat(ld)
 
 
+def _all_gather_rows(t, group=None):
+    """All-gather equal-shaped [rows, ...] tensors into [world * rows, ...] (rank-major)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = t.contiguous()
+    if t.is_cuda and dist.get_backend(group) == "nccl":
+        out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype,
+                          device=t.device)
+        dist.all_gather_into_tensor(out, t, group=group)
+        return out
+    host = t.cpu()
+    parts = [torch.empty_like(host) for _ in range(world)]
+    dist.all_gather(parts, host, group=group)
+    return torch.cat(parts).to(t.device)
+
+
+def shard_bounds(B: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous query shard of rank `rank`: rows [lo, hi) of a B-query batch
+    (equal ceil(B / world) shards, the last ones possibly short or empty)."""
+    per = -(-B // world)
+    lo = min(B, rank * per)
+    return lo, min(B, lo + per)
+
+
+def sharded_search(dev_index, Q, params, source, cache=None, max_inflight: int = 0,
+                   group=None):
+    """One multi-GPU search step: every rank holds the replicated
+    index and the full query batch ``Q`` (CUDA float32 [B, dim]), searches its
+    contiguous shard with lv_search_batch, and the shards' ids, scores and
+    counters are all-gathered — the only collective. Returns CUDA tensors
+    ids [B, k], dist [B, k], counters [B, 4], identical on every rank and
+    identical to a single-rank search of the whole batch (per-query results do
+    not depend on batching, SURVEY 0 finding 1)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    B, k = Q.shape[0], params.k
+    lo, hi = shard_bounds(B, rank, world)
+    per = -(-B // world)
+    ids = torch.full((per, k), -1, dtype=torch.int64, device=Q.device)
+    dst = torch.zeros((per, k), dtype=torch.float32, device=Q.device)
+    cnt = torch.zeros((per, 4), dtype=torch.int64, device=Q.device)
+    if hi > lo:
+        out = dev_index.search_device(Q[lo:hi].contiguous(), params, source, cache=cache,
+                                      max_inflight=max_inflight)
+        ids[:hi - lo] = out["ids"][:hi - lo]
+        dst[:hi - lo] = out["dist"][:hi - lo]
+        cnt[:hi - lo] = out["counters"][:hi - lo]
+    if world == 1:
+        return ids[:B], dst[:B], cnt[:B]
+    return (_all_gather_rows(ids, group)[:B], _all_gather_rows(dst, group)[:B],
+            _all_gather_rows(cnt, group)[:B])
+
+
 def max_over_ranks(value: float, device=None, group=None) -> float:
     """The slowest rank's time (multi-GPU numbers are max over ranks)."""
     import torch

@@ -78,30 +78,93 @@ class MatrixSource:
     def __init__(self, matrix) -> None:
         self.matrix = matrix
 
+    def fetch(self, ids, report=None) -> np.ndarray:
+        """search.py:89-93 (host rows; the device path reads the matrix in HBM)."""
+        m = self.matrix
+        if hasattr(m, "data_ptr"):
+            import torch
+            return m[torch.as_tensor(list(ids), dtype=torch.int64, device=m.device)].cpu().numpy()
+        return np.asarray(m)[list(ids)]
+
 
 class ProviderSource:
-    """Recompute source (search.py:96-110): the attached GPU encoder embeds the
-    token payloads of the requested nodes. ``provider`` must be an
-    :class:`paper_2506_08276_b200.encoder.EncoderProvider` bound to the
-    index's token store."""
+    """Recompute source (search.py:96-110). With our
+    :class:`paper_2506_08276_b200.encoder.EncoderProvider` the GPU encoder embeds
+    the token rows of the requested nodes inside the device loop. Any other
+    provider (e.g. the reference's own ``SyntheticProvider``) is a HOST provider:
+    the device traversal calls :meth:`fetch` once per iteration with the new ids
+    of every in-flight query (``LV_SOURCE_CALLBACK``)."""
 
     def __init__(self, provider, payload_of=None) -> None:
         self.provider = provider
         self.payload_of = payload_of
 
+    def fetch(self, ids, report=None) -> np.ndarray:
+        """search.py:103-110: payload fetch + ``embed_all`` of the provider."""
+        if hasattr(self.provider, "embed_batch") and self.payload_of is not None:
+            requests = [_EmbeddingRequest(int(i), self.payload_of(int(i))) for i in ids]
+            mb = int(getattr(getattr(self.provider, "config", None), "max_batch", 0) or
+                     len(requests) or 1)
+            rows = [np.asarray(self.provider.embed_batch(requests[j:j + mb]), dtype=np.float32)
+                    for j in range(0, len(requests), mb)]
+            return np.concatenate(rows) if rows else np.empty((0, 0), np.float32)
+        raise InvalidArgumentError("provider has no host embed path")
+
+
+@dataclass(frozen=True)
+class _EmbeddingRequest:
+    """vectors.py:33-38 (item_id, content)."""
+
+    item_id: int
+    content: bytes
+
 
 class EmbeddingCache:
-    """Pinned exact vectors of the highest-degree nodes (search.py:113-142)."""
+    """Pinned exact vectors of the highest-degree nodes (search.py:113-142).
 
-    def __init__(self, ids) -> None:
+    Built from ids (the device encoder computes the pinned rows once) or, like
+    the reference, from ``vectors: {id: row}``."""
+
+    def __init__(self, ids=None, vectors: dict | None = None) -> None:
+        if vectors is not None:
+            ids = vectors.keys()
         self.ids = np.asarray(sorted(int(i) for i in ids), dtype=np.int64)
         self._set = set(self.ids.tolist())
+        self.vectors = vectors
 
     def __len__(self) -> int:
         return len(self.ids)
 
     def __contains__(self, node_id: int) -> bool:
         return node_id in self._set
+
+
+def _cache_ids(cache) -> np.ndarray:
+    """Sorted ids of our cache or the reference's (``.vectors`` dict)."""
+    if hasattr(cache, "ids"):
+        return np.ascontiguousarray(cache.ids, dtype=np.int64)
+    return np.asarray(sorted(int(i) for i in cache.vectors), dtype=np.int64)
+
+
+def _cache_rows(cache, ids: np.ndarray):
+    vec = getattr(cache, "vectors", None)
+    if not vec:
+        return None
+    return np.ascontiguousarray(np.stack([np.asarray(vec[int(i)], dtype=np.float32)
+                                          for i in ids]))
+
+
+def _source_kind(source) -> str:
+    """matrix | encoder | callback — duck-typed like the reference (search.py:78-110)."""
+    prov = getattr(source, "provider", None)
+    if prov is None and hasattr(source, "matrix"):
+        return "matrix"
+    if prov is not None and hasattr(prov, "attach"):
+        return "encoder"
+    if hasattr(source, "fetch"):
+        return "callback"
+    raise InvalidArgumentError(
+        "source must be MatrixSource, ProviderSource or an object with fetch(ids, report)")
 
 
 def build_embedding_cache(graph, fraction_percent: float, source=None) -> EmbeddingCache:
@@ -122,6 +185,44 @@ def query_norm(q: np.ndarray) -> np.float32:
 
 def query_norms(Q: np.ndarray) -> np.ndarray:
     return np.array([query_norm(q) for q in Q], dtype=np.float32)
+
+
+def device_query_norms(Q):
+    """The same norms computed on the device in the OpenBLAS sdot order
+    (lv_numerics.cuh ``sdot_openblas``): bit-identical to :func:`query_norms`
+    on a SkylakeX-kernel BLAS host for dim % 32 == 0. CUDA tensor in -> out."""
+    import torch
+    Q = Q.contiguous()
+    out = torch.empty(Q.shape[0], dtype=torch.float32, device=Q.device)
+    _lib.check(_lib.lib().lv_query_norms(Q.data_ptr(), Q.shape[0], Q.shape[1], out.data_ptr(),
+                                         _lib.LV_IO_DEVICE,
+                                         torch.cuda.current_stream(Q.device).cuda_stream))
+    return out
+
+
+def as_pruned(graph):
+    """The CSR the device loads: a PrunedGraph (ours or the reference's), or the
+    reference's ``OverlayGraph`` (update.py:93-191, what ``Engine.search``
+    passes, index.py:315) — its base when nothing is overridden, else a frozen
+    snapshot (``OverlayGraph.freeze``) cached on the overlay by content."""
+    if hasattr(graph, "level_offsets"):
+        return graph
+    if hasattr(graph, "overrides") and hasattr(graph, "base"):
+        base = graph.base
+        deleted = np.asarray(getattr(graph, "_deleted", base.deleted if base is not None else []),
+                             dtype=bool)
+        if base is not None and graph.n == base.n and not any(graph.overrides):
+            return base   # mark_deleted keeps base.deleted in step (update.py:156-161)
+        key = (graph.n, graph.entry_point,
+               tuple((lvl, v, tuple(row)) for lvl, d in enumerate(graph.overrides)
+                     for v, row in sorted(d.items())))
+        snap = graph.__dict__.get("_lv_frozen")
+        if snap is None or snap[0] != key:
+            snap = (key, graph.freeze(graph.max_degree))
+            graph.__dict__["_lv_frozen"] = snap
+        snap[1].deleted = deleted
+        return snap[1]
+    raise InvalidArgumentError("graph must be a PrunedGraph or an OverlayGraph")
 
 
 # --------------------------------------------------------------------------- device index
@@ -180,10 +281,11 @@ class DeviceIndex:
         handle = C.c_void_p()
         _lib.check(L.lv_index_create(C.byref(d), device, C.byref(handle)))
         self.handle = handle
-        self._matrix_key = None
         self._matrix_ref = None
-        self._cache_key = None
+        self._cache_ref = None   # the cache object whose ids/rows are on the device
+        self._cache_rows_set = False
         self._encoder = None
+        self._fetch = None
 
     @classmethod
     def for_pq(cls, model) -> "DeviceIndex":
@@ -217,8 +319,7 @@ class DeviceIndex:
                                                     else None, 0))
 
     def set_matrix(self, matrix) -> None:
-        key = id(matrix)
-        if key == self._matrix_key:
+        if matrix is self._matrix_ref:   # strong reference held: identity is safe
             return
         if hasattr(matrix, "data_ptr"):
             if tuple(matrix.shape) != (self.n, self.dim) or str(matrix.dtype) != "torch.float32":
@@ -230,7 +331,6 @@ class DeviceIndex:
             if m.shape != (self.n, self.dim):
                 raise InvalidArgumentError(f"matrix shape {m.shape} != ({self.n}, {self.dim})")
             _lib.check(_lib.lib().lv_index_set_matrix(self.handle, m.ctypes.data, 0))
-        self._matrix_key = key
         self._matrix_ref = matrix
 
     def attach_encoder(self, provider) -> None:
@@ -238,17 +338,92 @@ class DeviceIndex:
             return
         provider.attach(self)
         self._encoder = provider
-        self._cache_key = None
+        self._cache_ref = None
 
-    def set_cache(self, cache: EmbeddingCache | None) -> None:
-        key = None if cache is None else id(cache)
-        if key == self._cache_key:
+    def set_cache(self, cache, source_kind: str = "encoder", source=None) -> None:
+        """Device copy of an EmbeddingCache (ours or the reference's). The
+        cache object is held, so identity comparison cannot alias a freed one.
+        Pinned rows: the reference cache's ``vectors`` when present, else the
+        attached encoder's (encoder source) or ``source.fetch`` (host provider)."""
+        if cache is self._cache_ref and (cache is None or source_kind == "matrix"
+                                         or self._cache_rows_set):
             return
-        ids = None if cache is None else np.ascontiguousarray(cache.ids, dtype=np.int64)
+        ids = None if cache is None else _cache_ids(cache)
         _lib.check(_lib.lib().lv_index_set_cache(
             self.handle, None if ids is None else ids.ctypes.data,
             0 if ids is None else ids.shape[0], 0))
-        self._cache_key = key
+        self._cache_ref = cache
+        self._cache_rows_set = source_kind == "encoder" and self._encoder is not None
+        if cache is None or source_kind == "matrix" or not len(ids):
+            return
+        rows = _cache_rows(cache, ids)
+        if rows is None and source_kind == "callback":
+            rows = np.ascontiguousarray(source.fetch(ids.tolist(), SearchReport()),
+                                        dtype=np.float32)
+        if rows is not None:
+            if rows.shape != (ids.shape[0], self.dim):
+                raise InvalidArgumentError("cache vectors do not match the index dim")
+            _lib.check(_lib.lib().lv_index_set_cache_rows(self.handle, rows.ctypes.data, 0))
+            self._cache_rows_set = True
+
+    def _bind_source(self, source, p, dry_matrix=None) -> str:
+        """Point the device at the source; returns its kind."""
+        kind = _source_kind(source)
+        if kind == "matrix":
+            p.source = _lib.LV_SOURCE_MATRIX
+            self.set_matrix(source.matrix)
+        elif kind == "encoder":
+            p.source = _lib.LV_SOURCE_ENCODER
+            if dry_matrix is not None:
+                p.flags |= _lib.LV_DRY_RECOMPUTE
+                self.set_matrix(dry_matrix)
+            else:
+                self.attach_encoder(source.provider)
+        else:
+            p.source = _lib.LV_SOURCE_CALLBACK
+        return kind
+
+    def _install_fetch(self, source, report: "SearchReport", errors: list):
+        """ctypes trampoline: lv_fetch_fn -> source.fetch(ids, report)."""
+        dim = self.dim
+
+        def fn(_user, ids_p, n, rows_p):
+            try:
+                ids = np.ctypeslib.as_array(ids_p, shape=(n,)).tolist()
+                rows = np.asarray(source.fetch(ids, report), dtype=np.float32)
+                if rows.shape != (n, dim):
+                    raise InvalidArgumentError(
+                        f"provider returned {rows.shape}, expected ({n}, {dim})")
+                np.ctypeslib.as_array(rows_p, shape=(n, dim))[...] = rows
+                return 0
+            except BaseException as exc:   # surfaced after the call (LV_ERR_PROVIDER)
+                errors.append(exc)
+                return 1
+
+        cfn = _lib.FETCH_FN(fn)
+        _lib.check(_lib.lib().lv_index_set_fetch(self.handle, cfn, None))
+        self._fetch = cfn   # keep the trampoline alive
+        return cfn
+
+    def _run(self, call, kind, source, report):
+        """Run lv_search_batch; a host-provider failure becomes SearchError
+        with the partial report (search.py:169-172)."""
+        errors: list = []
+        if kind == "callback":
+            self._install_fetch(source, report, errors)
+        try:
+            rc = call()
+        finally:
+            if kind == "callback":
+                _lib.lib().lv_index_set_fetch(self.handle, _lib.FETCH_FN(0), None)
+                self._fetch = None
+        if rc != 0 and errors:
+            from .errors import ProviderError, SearchError
+            exc = errors[0]
+            if isinstance(exc, ProviderError) or type(exc).__name__ == "ProviderError":
+                raise SearchError(str(exc), partial_report=report) from exc
+            raise exc
+        _lib.check(rc)
 
     # -- ADC / distances (pq.py:153-189, vectors.py:120-140)
     def adc_tables(self, Q: np.ndarray, qn: np.ndarray) -> np.ndarray:
@@ -292,17 +467,8 @@ class DeviceIndex:
         p.mode = _lib.LV_MODE[params.mode]
         p.max_inflight = max_inflight
         p.flags = 0 if shared_recompute else _lib.LV_NO_SHARED_RECOMPUTE
-        if isinstance(source, MatrixSource):
-            p.source = _lib.LV_SOURCE_MATRIX
-            self.set_matrix(source.matrix)
-        elif isinstance(source, ProviderSource):
-            p.source = _lib.LV_SOURCE_ENCODER
-            self.attach_encoder(source.provider)
-        else:
-            raise InvalidArgumentError(
-                "source must be MatrixSource or ProviderSource(EncoderProvider); "
-                "the device path has no CPU fallback")
-        self.set_cache(cache)
+        kind = self._bind_source(source, p)
+        self.set_cache(cache, kind, source)
         p.use_cache = 1 if cache is not None else 0
         k = params.k
         ids = np.empty((B, k), dtype=np.int64)
@@ -323,8 +489,10 @@ class DeviceIndex:
             vis_cap = max(256, 4 * params.ef + 256)
             vis = np.empty((B, vis_cap), dtype=np.int32)
             o.visits, o.visits_cap = vis.ctypes.data, vis_cap
-        _lib.check(_lib.lib().lv_search_batch(self.handle, Q.ctypes.data, qn.ctypes.data, B,
-                                              C.byref(p), C.byref(o), stream))
+        scratch = SearchReport()
+        self._run(lambda: _lib.lib().lv_search_batch(self.handle, Q.ctypes.data, qn.ctypes.data,
+                                                      B, C.byref(p), C.byref(o), stream),
+                  kind, source, scratch)
         wall = time.perf_counter() - t0
         reports = []
         for b in range(B):
@@ -376,19 +544,8 @@ class DeviceIndex:
         p.mode = _lib.LV_MODE[params.mode]
         p.max_inflight = max_inflight
         p.flags = _lib.LV_IO_DEVICE | (0 if shared_recompute else _lib.LV_NO_SHARED_RECOMPUTE)
-        if isinstance(source, MatrixSource):
-            p.source = _lib.LV_SOURCE_MATRIX
-            self.set_matrix(source.matrix)
-        elif isinstance(source, ProviderSource) and dry_matrix is not None:
-            p.source = _lib.LV_SOURCE_ENCODER
-            p.flags |= _lib.LV_DRY_RECOMPUTE
-            self.set_matrix(dry_matrix)
-        elif isinstance(source, ProviderSource):
-            p.source = _lib.LV_SOURCE_ENCODER
-            self.attach_encoder(source.provider)
-        else:
-            raise InvalidArgumentError("source must be MatrixSource or ProviderSource")
-        self.set_cache(cache)
+        kind = self._bind_source(source, p, dry_matrix)
+        self.set_cache(cache, kind, source)
         p.use_cache = 1 if cache is not None else 0
         dev = Q.device
         if out is None or out["ids"].shape[0] < B or out["ids"].shape[1] != k:
@@ -403,8 +560,9 @@ class DeviceIndex:
         o.status = out["status"].data_ptr()
         st = torch.cuda.current_stream(dev).cuda_stream
         qp = None if qn is None else qn.data_ptr()
-        _lib.check(_lib.lib().lv_search_batch(self.handle, Q.data_ptr(), qp, B, C.byref(p),
-                                              C.byref(o), st))
+        self._run(lambda: _lib.lib().lv_search_batch(self.handle, Q.data_ptr(), qp, B,
+                                                      C.byref(p), C.byref(o), st),
+                  kind, source, SearchReport())
         return out
 
     def last_stats(self) -> dict:
@@ -415,13 +573,18 @@ class DeviceIndex:
 
 def device_index_for(graph, pq_model=None, pq_codes=None, metric=None,
                      dim=None) -> DeviceIndex:
-    """Per-(graph, PQ) cached DeviceIndex (the index is immutable, graph.py:32)."""
-    cache = graph.__dict__.setdefault("_lv_device", {})
-    key = (id(pq_model), id(pq_codes), metric, dim)
-    dev = cache.get(key)
-    if dev is None:
+    """Per-(graph, PQ) cached DeviceIndex (the index is immutable, graph.py:32).
+    Entries hold the PQ objects they were built from and match by identity, so
+    a retrained model can never reuse a freed object's device copy."""
+    graph = as_pruned(graph)
+    entries = graph.__dict__.setdefault("_lv_device", [])
+    for e in entries:
+        if e[0] is pq_model and e[1] is pq_codes and e[2] == metric and e[3] == dim:
+            dev = e[4]
+            break
+    else:
         dev = DeviceIndex(graph, pq_model, pq_codes, metric, dim=dim)
-        cache[key] = dev
+        entries.append((pq_model, pq_codes, metric, dim, dev))
     dev.sync_deleted(graph.deleted)
     return dev
 
@@ -434,6 +597,7 @@ def search_batch(graph, Q, params: SearchParams, source, metric: str, pq_model=N
     """Batched ``run_search``: all queries traverse concurrently on the device."""
     if params.mode == "two_level" and (pq_model is None or pq_codes is None):
         raise InvalidArgumentError("two_level mode requires PQ artifacts")
+    graph = as_pruned(graph)
     if pq_model is not None and pq_model.metric != metric:
         raise InvalidArgumentError("metric differs from the PQ model's metric")
     Q = np.asarray(Q, dtype=np.float32)
@@ -467,3 +631,40 @@ def best_first_search(graph, q, params: SearchParams, source, metric: str,
         params = SearchParams(params.k, params.ef, params.rerank_percent, params.batch_size,
                               "exact_bestfirst", params.cache_percent)
     return run_search(graph, q, params, source, metric, None, None, cache)
+
+
+def merge_pending(reports: list, Q, pending_ids, pending_vectors, metric: str, k: int,
+                  qn=None) -> list:
+    """``Engine.search``'s merge of the buffered (not yet inserted) items
+    (index.py:320-327 over ``MutableIndex.buffer_scan``, update.py:483-488):
+    distance() of each query to every pending vector (vectors.py:94-116, the
+    np.dot order) on the device, merged with the graph results by (distance,
+    id), first k kept. Updates and returns ``reports``."""
+    _lib.require_device()
+    pid = np.ascontiguousarray(pending_ids, dtype=np.int64).reshape(-1)
+    if pid.size == 0 or not reports:
+        return reports
+    pv = np.ascontiguousarray(pending_vectors, dtype=np.float32).reshape(pid.shape[0], -1)
+    Q = np.ascontiguousarray(Q, dtype=np.float32).reshape(len(reports), -1)
+    if Q.shape[1] != pv.shape[1]:
+        raise InvalidArgumentError(f"dimension mismatch: {Q.shape[1]} vs {pv.shape[1]}")
+    B = len(reports)
+    ids = np.full((B, k), -1, np.int64)
+    dist = np.zeros((B, k), np.float32)
+    count = np.zeros(B, np.int32)
+    for b, rep in enumerate(reports):
+        res = rep.results[:k]
+        count[b] = len(res)
+        for j, (i, d) in enumerate(res):
+            ids[b, j], dist[b, j] = i, d
+    qn_p = None
+    if qn is not None:
+        qn = np.ascontiguousarray(qn, dtype=np.float32)
+        qn_p = qn.ctypes.data
+    _lib.check(_lib.lib().lv_merge_pending(
+        _lib.LV_METRIC[metric], pv.ctypes.data, pid.ctypes.data, pid.shape[0], pv.shape[1],
+        Q.ctypes.data, qn_p, B, k, ids.ctypes.data, dist.ctypes.data, count.ctypes.data, 0,
+        None))
+    for b, rep in enumerate(reports):
+        rep.results = [(int(ids[b, j]), float(dist[b, j])) for j in range(int(count[b]))]
+    return reports

@@ -8,7 +8,8 @@ Usage: python tests/golden/make_encoder_golden.py
 3. Index built by the UNMODIFIED reference builder from those embeddings
    (the steps of build_index, builder.py:499-548, minus embed_items).
 4. The reference's own run_search (search.py:434-443) with
-   MatrixSource(embeddings) for every query; results and counters saved.
+   MatrixSource(embeddings) for every query; results and counters saved, with
+   the reference's ground truth and recall (evaluation.py:82-118).
 
 The GPU test (tests/test_gpu_encoder_parity.py) re-embeds the same token rows
 with the GPU fp32 encoder inside the recompute path and must return the same
@@ -32,6 +33,7 @@ from slimvec.builder import (BuildParams, assign_level, build_graph,  # noqa: E4
                              select_hubs, train_and_encode_pq)
 from slimvec.graph import save_graph  # noqa: E402
 from slimvec.pq import save_pq  # noqa: E402
+from slimvec.evaluation import ground_truth, mean_recall  # noqa: E402
 from slimvec.search import MatrixSource, SearchParams, run_search  # noqa: E402
 
 from oracle.encoder_ref import RefEncoder  # noqa: E402
@@ -39,7 +41,7 @@ from paper_2506_08276_b200.encoder import EncoderConfig, init_weights, lda_token
 
 OUT = Path(__file__).resolve().parent / "enc_fp32"
 CFG = EncoderConfig("golden-4l-d256", 4, 256, 4, 1024, 30522, 128)
-N, NQ, S, SEED = 2000, 100, 64, 11
+N, NQ, S, SEED = 2000, 1000, 64, 11
 PARAMS = [dict(k=3, ef=32, rerank_percent=30.0), dict(k=3, ef=64, rerank_percent=100.0)]
 
 
@@ -64,6 +66,7 @@ def main() -> None:
     np.save(OUT / "qtokens.npy", qtok)
     np.save(OUT / "embeddings_ref.npy", E)
     np.save(OUT / "queries_ref.npy", Q)
+    gt = ground_truth(E, Q, 3, "cosine")   # evaluation.py:98-105
     cases = []
     for p in PARAMS:
         reps = []
@@ -72,8 +75,10 @@ def main() -> None:
             reps.append(dict(ids=[int(i) for i, _ in r.results],
                              dist=[float(d) for _, d in r.results],
                              recomputations=r.recomputations, approx_lookups=r.approx_lookups))
-        cases.append(dict(params=p, reports=reps))
-    meta = dict(encoder=CFG.__dict__, n=N, n_queries=NQ, seq_len=S, seed=SEED, cases=cases)
+        cases.append(dict(params=p, recall=mean_recall([r["ids"] for r in reps], gt),
+                          reports=reps))
+    meta = dict(encoder=CFG.__dict__, n=N, n_queries=NQ, seq_len=S, seed=SEED,
+                ground_truth=gt.ids, cases=cases)
     (OUT / "reference_results.json").write_text(json.dumps(meta))
     print("wrote", OUT)
 

@@ -75,3 +75,12 @@ def test_world_size_2_gather_matches_single_process():
         assert np.array_equal(g_d, d.numpy())
     assert t == 11.0
     assert s == [1.0, 2.0]
+
+
+def test_shard_bounds_cover_uneven_batches():
+    from paper_2506_08276_b200.dist import shard_bounds
+    for B in (0, 1, 7, 101, 4096):
+        for world in (1, 2, 3, 8):
+            spans = [shard_bounds(B, r, world) for r in range(world)]
+            rows = [i for lo, hi in spans for i in range(lo, hi)]
+            assert rows == list(range(B))

@@ -145,3 +145,64 @@ def test_oracle_matches_reference_on_encoder_fixture():
             assert [i for i, _ in rep.results] == exp["ids"]
             assert [float(x) for _, x in rep.results] == exp["dist"]
             assert rep.recomputations == exp["recomputations"]
+
+
+@pytest.mark.parametrize("n", [32, 64, 96, 128, 256, 768, 1024])
+def test_sdot_order(n):
+    """np.dot of float32 vectors (OpenBLAS SkylakeX sdot) == the restated order
+    that lv_query_norms / lv_merge_pending run on the device."""
+    rng = np.random.default_rng(n)
+    for _ in range(60):
+        x = rng.standard_normal(n).astype(np.float32)
+        y = rng.standard_normal(n).astype(np.float32)
+        assert numerics.sdot_openblas(x, y).view(np.uint32) == np.dot(x, y).view(np.uint32)
+        assert numerics.sdot_openblas(x, x).view(np.uint32) == np.dot(x, x).view(np.uint32)
+
+
+def _engine_fixture():
+    import json
+    d = GOLDEN / "engine_pending"
+    g = sp.read_lgr1(d / "graph.bin")
+    g.deleted = sp.read_ldl1(d / "deleted.bin", g.n)
+    return dict(d=d, g=g, pq=sp.read_lpq1(d / "pq.bin"), matrix=np.load(d / "matrix.npy"),
+                pids=np.load(d / "pending_ids.npy"), pvec=np.load(d / "pending_vecs.npy"),
+                Q=np.load(d / "queries.npy"), meta=json.loads((d / "cases.json").read_text()))
+
+
+def test_oracle_engine_pending_merge():
+    """Engine.search with a pending buffer (index.py:305-328): oracle search +
+    oracle buffer_scan merge == the reference Engine's reports, bit for bit."""
+    fx = _engine_fixture()
+    src = sp.MatrixRows(fx["matrix"])
+    for case in fx["meta"]["cases"]:
+        prm = sp.SearchParams(**case["params"])
+        for q, exp in zip(fx["Q"], case["reports"]):
+            rep = sp.run_search(fx["g"], q, prm, src, fx["pq"]["metric"], fx["pq"]["codebooks"],
+                                fx["pq"]["codes"], qn=numerics.query_norm(q))
+            res = sp.merge_pending(rep.results, q, fx["pids"], fx["pvec"], "cosine", prm.k)
+            assert [i for i, _ in res] == exp["ids"]
+            assert [int(np.float32(d).view(np.uint32)) for _, d in res] == exp["dist"]
+            assert rep.recomputations == exp["recomputations"]
+
+
+def test_oracle_matches_reference_at_config1():
+    """Config-1 at full size (10k x 256-d, M=32, PQ m=32; make_c1_golden.py):
+    the oracle port reproduces the reference's ids, distance bits and
+    counters (first 40 queries of each case — CPU time)."""
+    import json
+    d = GOLDEN / "c1"
+    meta = json.loads((d / "reference_results.json").read_text())
+    g = sp.read_lgr1(d / "graph.bin")
+    pq = sp.read_lpq1(d / "pq.bin")
+    E, Q = np.load(d / "embeddings_ref.npy"), np.load(d / "queries_ref.npy")
+    src = sp.MatrixRows(E)
+    for case in meta["cases"]:
+        prm = sp.SearchParams(**case["params"])
+        for q, exp in list(zip(Q, case["reports"]))[:40]:
+            rep = sp.run_search(g, q, prm, src, "cosine", pq["codebooks"], pq["codes"],
+                                qn=numerics.query_norm(q))
+            assert [i for i, _ in rep.results] == exp["ids"]
+            assert [np.float32(x).view(np.uint32) for _, x in rep.results] == \
+                [np.float32(x).view(np.uint32) for x in exp["dist"]]
+            assert rep.recomputations == exp["recomputations"]
+            assert rep.approx_lookups == exp["approx_lookups"]
