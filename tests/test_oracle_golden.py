@@ -206,3 +206,27 @@ def test_oracle_matches_reference_at_config1():
                 [np.float32(x).view(np.uint32) for x in exp["dist"]]
             assert rep.recomputations == exp["recomputations"]
             assert rep.approx_lookups == exp["approx_lookups"]
+
+
+def test_oracle_matches_reference_at_config2_shape():
+    """Config-2 shape (100k x 768, GPU-built M=32 graph, PQ m=64;
+    make_c2shape_golden.py): the oracle port reproduces the reference's ids,
+    distance bits and counters (first 12 queries per case — CPU time)."""
+    import json
+    import sys
+    sys.path.insert(0, str(GOLDEN))
+    import c2shape
+    d = GOLDEN / "c2shape"
+    meta = json.loads((d / "reference_results.json").read_text())
+    g = sp.read_lgr1(d / "graph.bin")
+    pq = sp.read_lpq1(d / "pq.bin")
+    E, Q = c2shape.make()
+    src = sp.MatrixRows(E)
+    for case in meta["cases"]:
+        prm = sp.SearchParams(**case["params"])
+        for q, exp in list(zip(Q, case["reports"]))[:12]:
+            rep = sp.run_search(g, q, prm, src, "cosine", pq["codebooks"], pq["codes"],
+                                qn=numerics.query_norm(q))
+            assert [i for i, _ in rep.results] == exp["ids"]
+            assert [int(np.float32(x).view(np.uint32)) for _, x in rep.results] == exp["dist"]
+            assert rep.recomputations == exp["recomputations"]
