@@ -40,7 +40,8 @@
  *   lv_attention_bf16 / lv_attention_gqa_bf16
  *                        <- the encoder's attention (BERT-style MHA; config-4 causal GQA),
  *                           exported for unit tests of the tcgen05 attention kernels
- *   lv_encoder_set_fused_ln, lv_set_gemm_mode, lv_set_attention_mode
+ *   lv_encoder_set_fused_ln, lv_encoder_set_split_residual, lv_set_gemm_mode,
+ *   lv_set_attention_mode
  *                        <- kernel-variant switches for parity tests and A/B measurements
  *
  * Conventions: plain pointers and sizes only. Unless LV_IO_DEVICE is set in a
@@ -242,6 +243,10 @@ int lv_encoder_reset_stats(lv_encoder *enc);
 /* bf16 encoder: 1 = LayerNorms folded into the GEMM epilogues (default when
  * hidden, ffn % 256 == 0), 0 = standalone LayerNorm kernels. */
 int lv_encoder_set_fused_ln(lv_encoder *enc, int enable);
+/* bf16 encoder with fused LayerNorms: 1 (default) = the residual stream is carried
+ * as a (hi, lo) bf16 pair (~16-bit mantissa) through the residual GEMM epilogues and
+ * the pooling, 0 = bf16 residual stream. */
+int lv_encoder_set_split_residual(lv_encoder *enc, int enable);
 
 /* out[M][N] = epi(A[M][K] . W[N][K]^T (+ bias) ...), bf16 device pointers, fp32 bias;
  * epi: 0 bias, 1 bias + erf-GELU, 2 bias + residual. N % 128 == 0, K % 64 == 0. */

@@ -117,6 +117,7 @@ EXPORTS = {
     "lv_attention_gqa_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "lv_encoder_set_fused_ln": (C.c_int, [C.c_void_p, C.c_int]),
+    "lv_encoder_set_split_residual": (C.c_int, [C.c_void_p, C.c_int]),
     "lv_attention_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_int32, C.c_void_p]),
     "lv_encoder_stats": (C.c_int, [C.c_void_p, C.POINTER(EncoderStats)]),

@@ -56,7 +56,8 @@ __global__ void embed_ln_kernel(const void *__restrict__ tokens, int token_bytes
                                 const int32_t *__restrict__ ids, int64_t seq0, int64_t n_seqs,
                                 const float *__restrict__ tok_emb, const float *__restrict__ pos_emb,
                                 int vocab, const float *__restrict__ g,
-                                const float *__restrict__ b, int d, T *__restrict__ out) {
+                                const float *__restrict__ b, int d, T *__restrict__ out,
+                                T *__restrict__ out_lo = nullptr) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n_seqs * S) return;
@@ -94,7 +95,10 @@ __global__ void embed_ln_kernel(const void *__restrict__ tokens, int token_bytes
   for (int i = 0; i < 32; ++i)
     if (i < per) {
       const int c = i * 32 + lane;
-      o[c] = from_f<T>((v[i] - mean) * rstd * __ldg(g + c) + __ldg(b + c));
+      const float val = (v[i] - mean) * rstd * __ldg(g + c) + __ldg(b + c);
+      const T hi = from_f<T>(val);
+      o[c] = hi;
+      if (out_lo) out_lo[row * d + c] = from_f<T>(val - to_f<T>(hi));  // split residual stream
     }
 }
 
@@ -275,6 +279,7 @@ __global__ void ln_stats_finalize_kernel(const float2 *__restrict__ parts, int n
 // then L2 normalisation. One block per sequence; thread t owns columns
 // [8t, 8t + 8) (16-byte loads, d % 8 == 0, d <= 1024), fixed summation order.
 __global__ void __launch_bounds__(128) pool_ln_kernel(const __nv_bfloat16 *__restrict__ y,
+                                                      const __nv_bfloat16 *__restrict__ y_lo,
                                                       const float2 *__restrict__ st,
                                                       const float *__restrict__ g,
                                                       const float *__restrict__ b,
@@ -290,15 +295,21 @@ __global__ void __launch_bounds__(128) pool_ln_kernel(const __nv_bfloat16 *__res
   if (live) {
     const uint4 *base = reinterpret_cast<const uint4 *>(y + seq * S * d + c0);
     const int stride = d / 8;
+    const uint4 *base_lo =
+        y_lo ? reinterpret_cast<const uint4 *>(y_lo + seq * S * d + c0) : nullptr;
     for (int p = 0; p < S; ++p) {
       const uint4 u = __ldg(base + (size_t)p * stride);
       const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+      uint4 ul = make_uint4(0u, 0u, 0u, 0u);
+      if (base_lo) ul = __ldg(base_lo + (size_t)p * stride);  // split residual: y = hi + lo
+      const __nv_bfloat162 *hl = reinterpret_cast<const __nv_bfloat162 *>(&ul);
       const float mu = sst[p].x, rs = sst[p].y;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 f = __bfloat1622float2(h[e]);
-        acc[2 * e] = fmaf(f.x - mu, rs, acc[2 * e]);
-        acc[2 * e + 1] = fmaf(f.y - mu, rs, acc[2 * e + 1]);
+        const float2 fl = __bfloat1622float2(hl[e]);
+        acc[2 * e] = fmaf((f.x + fl.x) - mu, rs, acc[2 * e]);
+        acc[2 * e + 1] = fmaf((f.y + fl.y) - mu, rs, acc[2 * e + 1]);
       }
     }
   }
@@ -591,8 +602,10 @@ struct lv_encoder {
   // activation workspace (element size 2 or 4), grown on demand
   int64_t cap_tokens = 0;
   void *x = nullptr, *qkv = nullptr, *ctx = nullptr, *y = nullptr, *h = nullptr;
+  void *x_lo = nullptr, *y_lo = nullptr;  // split residual stream (low halves)
   float2 *st_part = nullptr, *st1 = nullptr, *st2 = nullptr;  // LN statistics (fused mode)
   bool fuse_ln = false;  // bf16: LayerNorms folded into the GEMM epilogues
+  bool split_res = true;  // fused bf16: residual stream as (hi, lo) bf16 pairs (EPF_SPLIT)
   // profiling of the dense GEMMs (lv_encoder_profile)
   bool profile = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -612,6 +625,8 @@ struct lv_encoder {
     cudaFree(ctx);
     cudaFree(y);
     cudaFree(h);
+    cudaFree(x_lo);
+    cudaFree(y_lo);
     cudaFree(st_part);
     cudaFree(st1);
     cudaFree(st2);
@@ -672,10 +687,12 @@ int ensure_ws(lv_encoder *e, int64_t tokens) {
   cudaFree(e->ctx);
   cudaFree(e->y);
   cudaFree(e->h);
+  cudaFree(e->x_lo);
+  cudaFree(e->y_lo);
   cudaFree(e->st_part);
   cudaFree(e->st1);
   cudaFree(e->st2);
-  e->x = e->qkv = e->ctx = e->y = e->h = nullptr;
+  e->x = e->qkv = e->ctx = e->y = e->h = e->x_lo = e->y_lo = nullptr;
   e->st_part = e->st1 = e->st2 = nullptr;
   e->cap_tokens = 0;
   const size_t es = e->esize();
@@ -692,6 +709,10 @@ int ensure_ws(lv_encoder *e, int64_t tokens) {
   LV_CHECK_CUDA(cudaMalloc(&e->ctx, tokens * w_ctx * es));
   LV_CHECK_CUDA(cudaMalloc(&e->y, tokens * d * es));
   LV_CHECK_CUDA(cudaMalloc(&e->h, tokens * w_h * es));
+  if (e->cfg.precision == 1 && e->cfg.arch == 0) {
+    LV_CHECK_CUDA(cudaMalloc(&e->x_lo, tokens * d * es));
+    LV_CHECK_CUDA(cudaMalloc(&e->y_lo, tokens * d * es));
+  }
   if (e->cfg.precision == 1) {
     LV_CHECK_CUDA(cudaMalloc(&e->st_part, tokens * (d / 64) * sizeof(float2)));
     LV_CHECK_CUDA(cudaMalloc(&e->st1, tokens * sizeof(float2)));
@@ -809,6 +830,8 @@ int forward_fused(lv_encoder *e, int64_t ns, int S, int M, float *out, cudaStrea
   const int d = c.hidden, ff = c.ffn, H = c.heads, dh = c.hidden / c.heads;
   using bf = __nv_bfloat16;
   bf *x = (bf *)e->x, *qkv = (bf *)e->qkv, *ctx = (bf *)e->ctx, *y = (bf *)e->y, *h = (bf *)e->h;
+  const bool split = e->split_res;
+  bf *x_lo = split ? (bf *)e->x_lo : nullptr, *y_lo = split ? (bf *)e->y_lo : nullptr;
   for (size_t l = 0; l < e->layers.size(); ++l) {
     const EncLayer &L = e->layers[l];
     const EncLayer *P = l ? &e->layers[l - 1] : nullptr;
@@ -826,8 +849,10 @@ int forward_fused(lv_encoder *e, int64_t ns, int S, int M, float *out, cudaStrea
     LV_TRY(timed_attention(e, qkv, ctx, (int)ns, S, H, dh, s));
     EpiParams o;
     o.bias = L.b_o;
-    o.flags = EPF_RES | EPF_STATS;
+    o.flags = EPF_RES | EPF_STATS | (split ? EPF_SPLIT : 0);
     o.stats = e->st_part;
+    o.res_lo = x_lo;
+    o.out_lo = y_lo;
     if (P) {
       o.flags |= EPF_RES_LN;
       o.res_ln = e->st2;
@@ -844,7 +869,9 @@ int forward_fused(lv_encoder *e, int64_t ns, int S, int M, float *out, cudaStrea
     LV_TRY(fused_gemm(e, y, L.w_1_f, nullptr, h, M, ff, d, f1, s));
     EpiParams f2;
     f2.bias = L.b_2;
-    f2.flags = EPF_RES | EPF_RES_LN | EPF_STATS;
+    f2.flags = EPF_RES | EPF_RES_LN | EPF_STATS | (split ? EPF_SPLIT : 0);
+    f2.res_lo = y_lo;
+    f2.out_lo = x_lo;
     f2.res_ln = e->st1;
     f2.res_g = L.ln1_g;
     f2.res_b = L.ln1_b;
@@ -853,7 +880,7 @@ int forward_fused(lv_encoder *e, int64_t ns, int S, int M, float *out, cudaStrea
     LV_TRY(finalize_stats(e, e->st2, M, s));
   }
   const EncLayer &Z = e->layers.back();
-  pool_ln_kernel<<<(unsigned)ns, 128, 0, s>>>(x, e->st2, Z.ln2_g, Z.ln2_b, out, S, d);
+  pool_ln_kernel<<<(unsigned)ns, 128, 0, s>>>(x, x_lo, e->st2, Z.ln2_g, Z.ln2_b, out, S, d);
   note_launch();
   LV_CHECK_CUDA(cudaGetLastError());
   return LV_OK;
@@ -871,9 +898,12 @@ int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int
   for (int64_t s0 = 0; s0 < n_seqs; s0 += chunk) {
     const int64_t ns = std::min(chunk, n_seqs - s0);
     const int M = (int)(ns * S);
+    T *x_lo = nullptr;
+    if constexpr (sizeof(T) == 2)
+      if (e->fuse_ln && e->split_res) x_lo = (T *)e->x_lo;
     embed_ln_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, s>>>(
         tokens, token_bytes, S, d_ids, s0, ns, e->tok_emb, e->pos_emb, c.vocab, e->emb_g,
-        e->emb_b, d, x);
+        e->emb_b, d, x, x_lo);
         note_launch();
     LV_CHECK_CUDA(cudaGetLastError());
     if constexpr (sizeof(T) == 2) {
@@ -1324,6 +1354,12 @@ int lv_set_gemm_mode(int mode) {
   g_short_k = (mode & 2) ? 1024 : 0;
   g_long_k_single = (mode & 4) ? 0 : 1;
   return prev;
+}
+
+int lv_encoder_set_split_residual(lv_encoder *enc, int enable) {
+  LV_REQUIRE(enc, LV_ERR_USAGE, "null encoder");
+  enc->split_res = enable != 0;
+  return LV_OK;
 }
 
 int lv_encoder_set_fused_ln(lv_encoder *enc, int enable) {

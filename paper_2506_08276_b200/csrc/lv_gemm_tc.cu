@@ -271,10 +271,14 @@ struct PairCfg {
   // kMode 3: SwiGLU epilogue (no residual; gate/up interleaved per 64 columns)
   // kMode 4: residual with a single box buffer and 5 stages (long-K GEMMs: the
   // epilogue has slack, the residual box is loaded when the box starts)
-  static constexpr bool kRes = kMode == 1 || kMode == 2 || kMode == 4;
-  static constexpr int kStages = (kMode == 0 || kMode == 3 || kMode == 4) ? 5 : kMode == 1 ? 4 : 3;
-  static constexpr int kBufs = (kMode == 0 || kMode == 3 || kMode == 4) ? 1 : kMode == 1 ? 2 : 3;
-  static constexpr int kStagingBytes = kEpiWarps * kBufs * kBoxBytes;
+  // kMode 5: split residual (EPF_SPLIT): one (hi, lo) box pair per warp, 4 stages
+  static constexpr bool kRes = kMode == 1 || kMode == 2 || kMode == 4 || kMode == 5;
+  static constexpr bool kSplit = kMode == 5;
+  static constexpr int kStages = (kMode == 0 || kMode == 3 || kMode == 4) ? 5
+                                 : (kMode == 1 || kMode == 5) ? 4 : 3;
+  static constexpr int kBufs = (kMode == 0 || kMode == 3 || kMode == 4 || kMode == 5) ? 1
+                               : kMode == 1 ? 2 : 3;
+  static constexpr int kStagingBytes = kEpiWarps * kBufs * kBoxBytes * (kSplit ? 2 : 1);
   static constexpr int kSmem = kStages * kStageBytes2 + kStagingBytes + kColVecTotal + 1024 + 512;
 };
 
@@ -326,7 +330,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmO,
-                        const __grid_constant__ CUtensorMap tmR, int M, int N, int K,
+                        const __grid_constant__ CUtensorMap tmR,
+                        const __grid_constant__ CUtensorMap tmRL,
+                        const __grid_constant__ CUtensorMap tmOL, int M, int N, int K,
                         const EpiParams ep) {
   constexpr int BN = 256;
   extern __shared__ uint8_t smem_raw[];
@@ -334,6 +340,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
   constexpr bool kRes = PairCfg<kMode>::kRes;
+  constexpr bool kSplit = PairCfg<kMode>::kSplit;
   constexpr int kBufs = PairCfg<kMode>::kBufs;
   constexpr int kStages2 = PairCfg<kMode>::kStages;
   constexpr int kStagingBytes = PairCfg<kMode>::kStagingBytes;
@@ -510,7 +517,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int half = ew >> 2;
     const int fl = ep.flags;
     constexpr bool has_res = kRes;
-    uint8_t *stg = sStage + ew * kBufs * kBoxBytes;
+    uint8_t *stg = sStage + ew * kBufs * kBoxBytes * (kSplit ? 2 : 1);  // kSplit: lo box after hi
+    constexpr uint32_t kResBytes = kBoxBytes * (kSplit ? 2 : 1);
     uint64_t *rb = rbar + 3 * ew;
     uint32_t rph = 0;  // parity bit per buffer
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
@@ -524,8 +532,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (has_res && lane == 0 && pair < num_tiles) {
       int x, y;
       box_coords(pair, 0, x, y);
-      mbar_expect_tx(&rb[0], kBoxBytes);
+      mbar_expect_tx(&rb[0], kResBytes);
       tma_load_2d(stg, &tmR, &rb[0], x, y, pol_r);
+      if constexpr (kSplit) tma_load_2d(stg + kBoxBytes, &tmRL, &rb[0], x, y, pol_r);
     }
     // column vectors of a box -> this warp's shared buffer, by cp.async (one
     // box ahead; reading them with per-chunk global loads exposed an L2 round
@@ -624,8 +633,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           } else if constexpr (kRes) {  // single buffer: this box's residual (box 0: prologue)
             if (blk > 0) {
               bulk_wait_read<0>();
-              mbar_expect_tx(&rb[0], kBoxBytes);
+              mbar_expect_tx(&rb[0], kResBytes);
               tma_load_2d(stg, &tmR, &rb[0], x, y, pol_r);
+              if constexpr (kSplit) tma_load_2d(stg + kBoxBytes, &tmRL, &rb[0], x, y, pol_r);
             }
           } else {
             bulk_wait_read<0>();  // the previous box's store has read the (single) buffer
@@ -662,6 +672,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = gelu_erf(v[e]);
           }
+          uint4 *cpl = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(cp) + kBoxBytes);
           if (has_res) {
             const uint4 u = *cp;
             const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
@@ -671,6 +682,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const float2 f = __bfloat1622float2(h[e]);
               rv[2 * e] = f.x;
               rv[2 * e + 1] = f.y;
+            }
+            if constexpr (kSplit) {  // residual = hi + lo
+              const uint4 ul = *cpl;
+              const __nv_bfloat162 *hl = reinterpret_cast<const __nv_bfloat162 *>(&ul);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(hl[e]);
+                rv[2 * e] += f.x;
+                rv[2 * e + 1] += f.y;
+              }
             }
             if (fl & EPF_RES_LN) {
               const float4 *g4 = reinterpret_cast<const float4 *>(cv + 128 + 8 * c);
@@ -690,7 +711,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           o.z = pack_bf16(v[4], v[5]);
           o.w = pack_bf16(v[6], v[7]);
           *cp = o;
-          if (fl & EPF_STATS) {
+          if constexpr (kSplit) {  // lo = bf16(v - hi); statistics of the unrounded v
+            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&o);
+            float lo[8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h[e]);
+              lo[2 * e] = v[2 * e] - f.x;
+              lo[2 * e + 1] = v[2 * e + 1] - f.y;
+            }
+            uint4 ol;
+            ol.x = pack_bf16(lo[0], lo[1]);
+            ol.y = pack_bf16(lo[2], lo[3]);
+            ol.z = pack_bf16(lo[4], lo[5]);
+            ol.w = pack_bf16(lo[6], lo[7]);
+            *cpl = ol;
+            if (fl & EPF_STATS) {
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                if (c == 0 && e == 0) sk = v[0];
+                const float a0 = v[e] - sk, a1 = v[e + 1] - sk;
+                s1 += a0 + a1;
+                s2 = fmaf(a0, a0, fmaf(a1, a1, s2));
+              }
+            }
+          } else if (fl & EPF_STATS) {
             const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&o);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -709,6 +754,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           tma_store_2d(&tmO, box, x, y);
+          if constexpr (kSplit) tma_store_2d(&tmOL, box + kBoxBytes, x, y);
           bulk_commit();
         }
       }
@@ -777,8 +823,19 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
              "cuTensorMapEncodeTiled(out) failed");
   LV_REQUIRE(make_tma_2d_bf16(&tr, residual ? residual : out, N, M, (uint64_t)N * 2, 64, 32),
              LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(residual) failed");
+  CUtensorMap trl = tr, tol = to;
+  const bool split = (ep.flags & EPF_SPLIT) != 0;
+  if (split) {
+    LV_REQUIRE(make_tma_2d_bf16(&trl, ep.res_lo, N, M, (uint64_t)N * 2, 64, 32), LV_ERR_INTERNAL,
+               "cuTensorMapEncodeTiled(residual lo) failed");
+    LV_REQUIRE(make_tma_2d_bf16(&tol, ep.out_lo, N, M, (uint64_t)N * 2, 64, 32), LV_ERR_INTERNAL,
+               "cuTensorMapEncodeTiled(out lo) failed");
+  }
   static bool attr_set = false;
   if (!attr_set) {
+    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<5>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PairCfg<5>::kSmem));
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<0>::kSmem));
@@ -800,23 +857,27 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
   const int pairs = std::min(tiles, tc_gemm_num_sms() / 2);
   const int mode = (ep.flags & EPF_SWIGLU) ? 3
                    : !(ep.flags & EPF_RES) ? 0
+                   : split ? 5
                    : K <= g_short_k ? 2
                    : (K > 1024 && g_long_k_single) ? 4 : 1;
-  if (mode == 4)
-    tc_gemm_pair_kernel<4><<<2 * pairs, kThreads, PairCfg<4>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
-                                                                          ep);
+  if (mode == 5)
+    tc_gemm_pair_kernel<5><<<2 * pairs, kThreads, PairCfg<5>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
+                                                                          M, N, K, ep);
+  else if (mode == 4)
+    tc_gemm_pair_kernel<4><<<2 * pairs, kThreads, PairCfg<4>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
+                                                                          M, N, K, ep);
   else if (mode == 3)
-    tc_gemm_pair_kernel<3><<<2 * pairs, kThreads, PairCfg<3>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
-                                                                          ep);
+    tc_gemm_pair_kernel<3><<<2 * pairs, kThreads, PairCfg<3>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
+                                                                          M, N, K, ep);
   else if (mode == 2)
-    tc_gemm_pair_kernel<2><<<2 * pairs, kThreads, PairCfg<2>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
-                                                                          ep);
+    tc_gemm_pair_kernel<2><<<2 * pairs, kThreads, PairCfg<2>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
+                                                                          M, N, K, ep);
   else if (mode == 1)
-    tc_gemm_pair_kernel<1><<<2 * pairs, kThreads, PairCfg<1>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
-                                                                          ep);
+    tc_gemm_pair_kernel<1><<<2 * pairs, kThreads, PairCfg<1>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
+                                                                          M, N, K, ep);
   else
-    tc_gemm_pair_kernel<0><<<2 * pairs, kThreads, PairCfg<0>::kSmem, s>>>(ta, tb, to, tr, M, N, K,
-                                                                          ep);
+    tc_gemm_pair_kernel<0><<<2 * pairs, kThreads, PairCfg<0>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
+                                                                          M, N, K, ep);
   note_launch();
   LV_CHECK_CUDA(cudaGetLastError());
   return LV_OK;
@@ -866,6 +927,9 @@ int tc_gemm_ex(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloat
   LV_REQUIRE(!(ep.flags & EPF_RES_LN) || (ep.res_ln && ep.res_g && ep.res_b), LV_ERR_USAGE,
              "tc_gemm_ex: residual LN needs statistics and affine");
   LV_REQUIRE(!(ep.flags & EPF_STATS) || ep.stats, LV_ERR_USAGE, "tc_gemm_ex: stats buffer");
+  LV_REQUIRE(!(ep.flags & EPF_SPLIT) || ((ep.flags & EPF_RES) && ep.res_lo && ep.out_lo &&
+                                         !(ep.flags & EPF_GELU)),
+             LV_ERR_USAGE, "tc_gemm_ex: split residual needs res_lo and out_lo");
   return launch_pair(A, W, residual, out, M, N, K, ep, s);
 }
 

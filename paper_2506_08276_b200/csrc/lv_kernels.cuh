@@ -33,10 +33,19 @@ struct TcGemmPlan;  // cached tensor maps for one (A, W, M, N, K)
 //   v += (res - mean_r) * rstd_r * res_g + res_b     (EPF_RES | EPF_RES_LN)
 //   stats[row][col / 64] = (mean, M2) of the bf16-rounded outputs of each
 //        64-column box (EPF_STATS; combined by ln_stats_finalize)
+//   EPF_SPLIT (with EPF_RES): the residual stream is carried at ~16-bit
+//        mantissa precision as a bf16 pair (hi, lo = bf16(v - hi)): the
+//        residual is res + res_lo, the output is written as out (hi) and
+//        out_lo, and the statistics are taken from the unrounded v. The
+//        consuming GEMMs read hi as their A operand; only the residual adds
+//        and the LayerNorm statistics see the pair. (Rounding the post-LN
+//        residual stream to bf16 at every sublayer was the dominant error of
+//        the bf16 encoder against the fp32 one.)
 //   out[:, j] = silu(acc[:, g(j)]) * acc[:, u(j)]   (EPF_SWIGLU, alone: weight
 //        rows interleaved per 64 as [gate 64 | up 64]; output width N / 2)
 enum EpiFlag : int {
-  EPF_GELU = 1, EPF_RES = 2, EPF_RES_LN = 4, EPF_LN_IN = 8, EPF_STATS = 16, EPF_SWIGLU = 32
+  EPF_GELU = 1, EPF_RES = 2, EPF_RES_LN = 4, EPF_LN_IN = 8, EPF_STATS = 16, EPF_SWIGLU = 32,
+  EPF_SPLIT = 64
 };
 struct EpiParams {
   const float *bias = nullptr;    // [N]
@@ -46,6 +55,8 @@ struct EpiParams {
   const float *res_g = nullptr;   // [N]  EPF_RES_LN
   const float *res_b = nullptr;   // [N]  EPF_RES_LN
   float2 *stats = nullptr;        // [M][N / 64]  EPF_STATS
+  const __nv_bfloat16 *res_lo = nullptr;  // [M][N]  EPF_SPLIT: low half of the residual
+  __nv_bfloat16 *out_lo = nullptr;        // [M][N]  EPF_SPLIT: low half of the output
   int flags = 0;
 };
 // 2-CTA kernel with the generalised epilogue; needs N % 256 == 0, K % 64 == 0.

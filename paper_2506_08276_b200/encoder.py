@@ -185,6 +185,12 @@ class GpuEncoder:
         run them as standalone kernels."""
         _lib.check(_lib.lib().lv_encoder_set_fused_ln(self.handle, 1 if enable else 0))
 
+    def set_split_residual(self, enable: bool) -> None:
+        """bf16 mode: carry the post-LN residual stream as a (hi, lo) bf16 pair
+        (default; ~16-bit mantissa, EPF_SPLIT) or round it to bf16 at every
+        sublayer (the earlier design, measurably further from fp32)."""
+        _lib.check(_lib.lib().lv_encoder_set_split_residual(self.handle, 1 if enable else 0))
+
     # -- device-timed GEMM counters (roofline evidence)
     def profile(self, enable: bool = True) -> None:
         _lib.check(_lib.lib().lv_encoder_profile(self.handle, 1 if enable else 0))

@@ -262,3 +262,25 @@ def test_decoder_encoder_batch_invariant(lv):
     whole = enc.encode(tok)
     parts = np.concatenate([enc.encode(tok[:3]), enc.encode(tok[3:])])
     assert np.array_equal(whole, parts)
+
+
+@pytest.mark.parametrize("name", ["small", "bert-base"])
+def test_split_residual_stream_is_closer_to_fp32(lv, name):
+    """The (hi, lo) bf16 residual stream (EPF_SPLIT, default) removes the
+    dominant bf16 error: its distance to the fp32 oracle is well below the
+    bf16-rounded stream's, and it stays batch-invariant."""
+    from oracle.encoder_ref import RefEncoder
+    from paper_2506_08276_b200.encoder import ENCODERS, GpuEncoder, init_weights, synthetic_tokens
+    cfg = _small_cfg(lv, layers=4) if name == "small" else ENCODERS["bert-base"]
+    w = init_weights(cfg, seed=31)
+    tok = synthetic_tokens(16, 128, cfg.vocab, seed=32)
+    ref = RefEncoder(cfg, w).encode(tok)
+    enc = GpuEncoder(cfg, w, precision="bf16")
+    split = enc.encode(tok)
+    assert np.array_equal(np.concatenate([enc.encode(tok[:5]), enc.encode(tok[5:])]), split)
+    enc.set_split_residual(False)
+    plain = enc.encode(tok)
+    err_split = np.linalg.norm(split - ref, axis=1).mean()
+    err_plain = np.linalg.norm(plain - ref, axis=1).mean()
+    print(f"{name}: |bf16 - fp32| split {err_split:.2e}, bf16 stream {err_plain:.2e}")
+    assert err_split < 0.7 * err_plain, (err_split, err_plain)
