@@ -244,8 +244,8 @@ int lv_encoder_reset_stats(lv_encoder *enc);
  * hidden, ffn % 256 == 0), 0 = standalone LayerNorm kernels. */
 int lv_encoder_set_fused_ln(lv_encoder *enc, int enable);
 /* bf16 encoder with fused LayerNorms: 1 (default) = the residual stream is carried
- * as a (hi, lo) bf16 pair (~16-bit mantissa) through the residual GEMM epilogues and
- * the pooling, 0 = bf16 residual stream. */
+ * as bf16 plus an int8 correction (~15-bit mantissa) through the residual GEMM
+ * epilogues and the pooling, 0 = bf16 residual stream. */
 int lv_encoder_set_split_residual(lv_encoder *enc, int enable);
 
 /* out[M][N] = epi(A[M][K] . W[N][K]^T (+ bias) ...), bf16 device pointers, fp32 bias;
@@ -266,7 +266,8 @@ int lv_attention_gqa_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S,
  * 1 = 1-CTA kernel only; + 2 = 3-buffer/3-stage epilogue for short-K residual GEMMs
  * (experiment; measured slower than the default 2-buffer/4-stage kernel); + 4 = the
  * 2-buffer/4-stage kernel also for long-K (K > 1024) residual GEMMs instead of the
- * default 1-buffer/5-stage one.
+ * default 1-buffer/5-stage one; + 8 = the 1-buffer/5-stage split-residual kernel also
+ * for short-K split-residual GEMMs (default: 2-buffer/3-stage).
  * Returns the previous mode. */
 int lv_set_gemm_mode(int mode);
 /* Attention kernel selection: 0 = auto (tcgen05/TMEM kernel for dh == 64 and

@@ -57,7 +57,7 @@ __global__ void embed_ln_kernel(const void *__restrict__ tokens, int token_bytes
                                 const float *__restrict__ tok_emb, const float *__restrict__ pos_emb,
                                 int vocab, const float *__restrict__ g,
                                 const float *__restrict__ b, int d, T *__restrict__ out,
-                                T *__restrict__ out_lo = nullptr) {
+                                int8_t *__restrict__ out_lo = nullptr) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n_seqs * S) return;
@@ -98,7 +98,7 @@ __global__ void embed_ln_kernel(const void *__restrict__ tokens, int token_bytes
       const float val = (v[i] - mean) * rstd * __ldg(g + c) + __ldg(b + c);
       const T hi = from_f<T>(val);
       o[c] = hi;
-      if (out_lo) out_lo[row * d + c] = from_f<T>(val - to_f<T>(hi));  // split residual stream
+      if (out_lo) out_lo[row * d + c] = (int8_t)lo8_encode(val, to_f<T>(hi));  // split stream
     }
 }
 
@@ -279,7 +279,7 @@ __global__ void ln_stats_finalize_kernel(const float2 *__restrict__ parts, int n
 // then L2 normalisation. One block per sequence; thread t owns columns
 // [8t, 8t + 8) (16-byte loads, d % 8 == 0, d <= 1024), fixed summation order.
 __global__ void __launch_bounds__(128) pool_ln_kernel(const __nv_bfloat16 *__restrict__ y,
-                                                      const __nv_bfloat16 *__restrict__ y_lo,
+                                                      const int8_t *__restrict__ y_lo,
                                                       const float2 *__restrict__ st,
                                                       const float *__restrict__ g,
                                                       const float *__restrict__ b,
@@ -295,21 +295,21 @@ __global__ void __launch_bounds__(128) pool_ln_kernel(const __nv_bfloat16 *__res
   if (live) {
     const uint4 *base = reinterpret_cast<const uint4 *>(y + seq * S * d + c0);
     const int stride = d / 8;
-    const uint4 *base_lo =
-        y_lo ? reinterpret_cast<const uint4 *>(y_lo + seq * S * d + c0) : nullptr;
+    const uint2 *base_lo =
+        y_lo ? reinterpret_cast<const uint2 *>(y_lo + seq * S * d + c0) : nullptr;
     for (int p = 0; p < S; ++p) {
       const uint4 u = __ldg(base + (size_t)p * stride);
       const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
-      uint4 ul = make_uint4(0u, 0u, 0u, 0u);
+      uint2 ul = make_uint2(0u, 0u);
       if (base_lo) ul = __ldg(base_lo + (size_t)p * stride);  // split residual: y = hi + lo
-      const __nv_bfloat162 *hl = reinterpret_cast<const __nv_bfloat162 *>(&ul);
+      const int8_t *q = reinterpret_cast<const int8_t *>(&ul);
       const float mu = sst[p].x, rs = sst[p].y;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 f = __bfloat1622float2(h[e]);
-        const float2 fl = __bfloat1622float2(hl[e]);
-        acc[2 * e] = fmaf((f.x + fl.x) - mu, rs, acc[2 * e]);
-        acc[2 * e + 1] = fmaf((f.y + fl.y) - mu, rs, acc[2 * e + 1]);
+        const float y0 = f.x + lo8_decode(q[2 * e]), y1 = f.y + lo8_decode(q[2 * e + 1]);
+        acc[2 * e] = fmaf(y0 - mu, rs, acc[2 * e]);
+        acc[2 * e + 1] = fmaf(y1 - mu, rs, acc[2 * e + 1]);
       }
     }
   }
@@ -602,7 +602,7 @@ struct lv_encoder {
   // activation workspace (element size 2 or 4), grown on demand
   int64_t cap_tokens = 0;
   void *x = nullptr, *qkv = nullptr, *ctx = nullptr, *y = nullptr, *h = nullptr;
-  void *x_lo = nullptr, *y_lo = nullptr;  // split residual stream (low halves)
+  void *x_lo = nullptr, *y_lo = nullptr;  // split residual stream: int8 corrections (lo8)
   float2 *st_part = nullptr, *st1 = nullptr, *st2 = nullptr;  // LN statistics (fused mode)
   bool fuse_ln = false;  // bf16: LayerNorms folded into the GEMM epilogues
   bool split_res = true;  // fused bf16: residual stream as (hi, lo) bf16 pairs (EPF_SPLIT)
@@ -709,9 +709,9 @@ int ensure_ws(lv_encoder *e, int64_t tokens) {
   LV_CHECK_CUDA(cudaMalloc(&e->ctx, tokens * w_ctx * es));
   LV_CHECK_CUDA(cudaMalloc(&e->y, tokens * d * es));
   LV_CHECK_CUDA(cudaMalloc(&e->h, tokens * w_h * es));
-  if (e->cfg.precision == 1 && e->cfg.arch == 0) {
-    LV_CHECK_CUDA(cudaMalloc(&e->x_lo, tokens * d * es));
-    LV_CHECK_CUDA(cudaMalloc(&e->y_lo, tokens * d * es));
+  if (e->cfg.precision == 1 && e->cfg.arch == 0) {  // int8 corrections of the split stream
+    LV_CHECK_CUDA(cudaMalloc(&e->x_lo, tokens * d));
+    LV_CHECK_CUDA(cudaMalloc(&e->y_lo, tokens * d));
   }
   if (e->cfg.precision == 1) {
     LV_CHECK_CUDA(cudaMalloc(&e->st_part, tokens * (d / 64) * sizeof(float2)));
@@ -831,7 +831,7 @@ int forward_fused(lv_encoder *e, int64_t ns, int S, int M, float *out, cudaStrea
   using bf = __nv_bfloat16;
   bf *x = (bf *)e->x, *qkv = (bf *)e->qkv, *ctx = (bf *)e->ctx, *y = (bf *)e->y, *h = (bf *)e->h;
   const bool split = e->split_res;
-  bf *x_lo = split ? (bf *)e->x_lo : nullptr, *y_lo = split ? (bf *)e->y_lo : nullptr;
+  int8_t *x_lo = split ? (int8_t *)e->x_lo : nullptr, *y_lo = split ? (int8_t *)e->y_lo : nullptr;
   for (size_t l = 0; l < e->layers.size(); ++l) {
     const EncLayer &L = e->layers[l];
     const EncLayer *P = l ? &e->layers[l - 1] : nullptr;
@@ -898,9 +898,9 @@ int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int
   for (int64_t s0 = 0; s0 < n_seqs; s0 += chunk) {
     const int64_t ns = std::min(chunk, n_seqs - s0);
     const int M = (int)(ns * S);
-    T *x_lo = nullptr;
+    int8_t *x_lo = nullptr;
     if constexpr (sizeof(T) == 2)
-      if (e->fuse_ln && e->split_res) x_lo = (T *)e->x_lo;
+      if (e->fuse_ln && e->split_res) x_lo = (int8_t *)e->x_lo;
     embed_ln_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, s>>>(
         tokens, token_bytes, S, d_ids, s0, ns, e->tok_emb, e->pos_emb, c.vocab, e->emb_g,
         e->emb_b, d, x, x_lo);
@@ -1349,10 +1349,12 @@ int lv_attention_gqa_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S,
 }
 
 int lv_set_gemm_mode(int mode) {
-  const int prev = g_gemm_mode | (g_short_k != 0 ? 2 : 0) | (g_long_k_single ? 0 : 4);
+  const int prev = g_gemm_mode | (g_short_k != 0 ? 2 : 0) | (g_long_k_single ? 0 : 4) |
+                   (g_split_single ? 8 : 0);
   g_gemm_mode = mode & 1;
   g_short_k = (mode & 2) ? 1024 : 0;
   g_long_k_single = (mode & 4) ? 0 : 1;
+  g_split_single = (mode & 8) ? 1 : 0;
   return prev;
 }
 

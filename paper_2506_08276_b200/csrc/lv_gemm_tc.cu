@@ -29,6 +29,7 @@
 namespace lv {
 int g_short_k = 0;  // residual GEMMs with K <= this use the 3-buffer epilogue (off: measured slower)
 int g_long_k_single = 1;  // residual GEMMs with K > 1024: single box buffer, 5 stages (kMode 4)
+int g_split_single = 0;   // split-residual GEMMs with K <= 1024: kMode 5 instead of 6
 namespace {
 
 constexpr int kBM = 128;
@@ -259,6 +260,7 @@ constexpr int kStageBytes2 = 2 * kHalfBytes;        // per CTA
 // epilogue staging: per epilogue warp two [32 rows][64 cols] bf16 boxes (4 KB
 // each, 128-byte swizzle) — residual tile in (TMA load), output tile out (TMA store)
 constexpr int kBoxBytes = 32 * 64 * 2;
+constexpr int kLoBoxBytes = 32 * 64;  // EPF_SPLIT: int8 [32 rows][64 cols], 64-byte swizzle
 // per epilogue warp, two boxes' column vectors (bias, colc, gamma, beta: 64 fp32 each)
 constexpr int kColVecBytes = 4 * 64 * 4;
 constexpr int kColVecTotal = kEpiWarps * 2 * kColVecBytes;
@@ -271,14 +273,18 @@ struct PairCfg {
   // kMode 3: SwiGLU epilogue (no residual; gate/up interleaved per 64 columns)
   // kMode 4: residual with a single box buffer and 5 stages (long-K GEMMs: the
   // epilogue has slack, the residual box is loaded when the box starts)
-  // kMode 5: split residual (EPF_SPLIT): one (hi, lo) box pair per warp, 4 stages
-  static constexpr bool kRes = kMode == 1 || kMode == 2 || kMode == 4 || kMode == 5;
-  static constexpr bool kSplit = kMode == 5;
-  static constexpr int kStages = (kMode == 0 || kMode == 3 || kMode == 4) ? 5
-                                 : (kMode == 1 || kMode == 5) ? 4 : 3;
+  // kMode 5: split residual (EPF_SPLIT), long K: one (hi bf16, lo int8) box
+  //          pair per warp, 5 stages
+  // kMode 6: split residual, short K: two box pairs (next box's residual
+  //          prefetched), 3 stages
+  static constexpr bool kRes = kMode == 1 || kMode == 2 || kMode == 4 || kMode >= 5;
+  static constexpr bool kSplit = kMode >= 5;
+  static constexpr int kStages = (kMode == 0 || kMode == 3 || kMode == 4 || kMode == 5) ? 5
+                                 : kMode == 1 ? 4 : 3;
   static constexpr int kBufs = (kMode == 0 || kMode == 3 || kMode == 4 || kMode == 5) ? 1
-                               : kMode == 1 ? 2 : 3;
-  static constexpr int kStagingBytes = kEpiWarps * kBufs * kBoxBytes * (kSplit ? 2 : 1);
+                               : (kMode == 1 || kMode == 6) ? 2 : 3;
+  static constexpr int kPairBytes = kBoxBytes + (kSplit ? kLoBoxBytes : 0);
+  static constexpr int kStagingBytes = kEpiWarps * kBufs * kPairBytes;
   static constexpr int kSmem = kStages * kStageBytes2 + kStagingBytes + kColVecTotal + 1024 + 512;
 };
 
@@ -517,8 +523,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int half = ew >> 2;
     const int fl = ep.flags;
     constexpr bool has_res = kRes;
-    uint8_t *stg = sStage + ew * kBufs * kBoxBytes * (kSplit ? 2 : 1);  // kSplit: lo box after hi
-    constexpr uint32_t kResBytes = kBoxBytes * (kSplit ? 2 : 1);
+    // per buffer: the bf16 box, then (kSplit) its int8 correction box
+    constexpr int kPair = PairCfg<kMode>::kPairBytes;
+    uint8_t *stg = sStage + ew * kBufs * kPair;
+    constexpr uint32_t kResBytes = kPair;
     uint64_t *rb = rbar + 3 * ew;
     uint32_t rph = 0;  // parity bit per buffer
     const uint32_t tempty_leader0 = map_to_rank(&tempty[0], 0);
@@ -577,7 +585,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int buf = blk & 1;            // column-vector buffer
         const int bb = blk % kBufs;         // epilogue box buffer
         const int nb = (blk + 1) % kBufs;   // the next box's buffer
-        uint8_t *box = stg + bb * kBoxBytes;
+        uint8_t *box = stg + bb * kPair;
+        uint8_t *lobox = box + kBoxBytes + (uint32_t)lane * 64;  // kSplit: this row's int8s
+        const uint32_t sw64 = (uint32_t)((lane >> 1) & 3);          // 64-byte swizzle of the row
+        uint4 lo_in = make_uint4(0u, 0u, 0u, 0u);
+        uint32_t lo_out[4] = {0u, 0u, 0u, 0u};
         int x, y;
         box_coords(tile, b, x, y);
         const int grow = y + lane;  // this thread's output row
@@ -627,8 +639,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               bulk_wait_read<kBufs - 2>();  // the store that last used buffer nb has read it
               int nx, ny;
               box_coords(nt, b ^ 1, nx, ny);
-              mbar_expect_tx(&rb[nb], kBoxBytes);
-              tma_load_2d(stg + nb * kBoxBytes, &tmR, &rb[nb], nx, ny, pol_r);
+              mbar_expect_tx(&rb[nb], kResBytes);
+              tma_load_2d(stg + nb * kPair, &tmR, &rb[nb], nx, ny, pol_r);
+              if constexpr (kSplit)
+                tma_load_2d(stg + nb * kPair + kBoxBytes, &tmRL, &rb[nb], nx, ny, pol_r);
             }
           } else if constexpr (kRes) {  // single buffer: this box's residual (box 0: prologue)
             if (blk > 0) {
@@ -672,7 +686,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = gelu_erf(v[e]);
           }
-          uint4 *cpl = reinterpret_cast<uint4 *>(reinterpret_cast<uint8_t *>(cp) + kBoxBytes);
+          // kSplit: the row's int8 corrections, 16 per 16-byte chunk (two column chunks)
+          uint4 *cpl = reinterpret_cast<uint4 *>(lobox + (((uint32_t)(c >> 1) ^ sw64) << 4));
+          if constexpr (kSplit)
+            if ((c & 1) == 0) lo_in = *cpl;
           if (has_res) {
             const uint4 u = *cp;
             const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
@@ -684,14 +701,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               rv[2 * e + 1] = f.y;
             }
             if constexpr (kSplit) {  // residual = hi + lo
-              const uint4 ul = *cpl;
-              const __nv_bfloat162 *hl = reinterpret_cast<const __nv_bfloat162 *>(&ul);
+              const int8_t *q = reinterpret_cast<const int8_t *>(&lo_in) + 8 * (c & 1);
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(hl[e]);
-                rv[2 * e] += f.x;
-                rv[2 * e + 1] += f.y;
-              }
+              for (int e = 0; e < 8; ++e) rv[e] += lo8_decode(q[e]);
             }
             if (fl & EPF_RES_LN) {
               const float4 *g4 = reinterpret_cast<const float4 *>(cv + 128 + 8 * c);
@@ -711,21 +723,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           o.z = pack_bf16(v[4], v[5]);
           o.w = pack_bf16(v[6], v[7]);
           *cp = o;
-          if constexpr (kSplit) {  // lo = bf16(v - hi); statistics of the unrounded v
+          if constexpr (kSplit) {  // int8 correction of hi; statistics of the unrounded v
             const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&o);
-            float lo[8];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f = __bfloat1622float2(h[e]);
-              lo[2 * e] = v[2 * e] - f.x;
-              lo[2 * e + 1] = v[2 * e + 1] - f.y;
+              const uint32_t q0 = (uint32_t)(lo8_encode(v[2 * e], f.x) & 0xff);
+              const uint32_t q1 = (uint32_t)(lo8_encode(v[2 * e + 1], f.y) & 0xff);
+              lo_out[2 * (c & 1) + (e >> 1)] |= (q0 | (q1 << 8)) << (16 * (e & 1));
             }
-            uint4 ol;
-            ol.x = pack_bf16(lo[0], lo[1]);
-            ol.y = pack_bf16(lo[2], lo[3]);
-            ol.z = pack_bf16(lo[4], lo[5]);
-            ol.w = pack_bf16(lo[6], lo[7]);
-            *cpl = ol;
+            if (c & 1) *cpl = make_uint4(lo_out[0], lo_out[1], lo_out[2], lo_out[3]);
+            if (c & 1) lo_out[0] = lo_out[1] = lo_out[2] = lo_out[3] = 0u;
             if (fl & EPF_STATS) {
 #pragma unroll
               for (int e = 0; e < 8; e += 2) {
@@ -826,9 +834,9 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
   CUtensorMap trl = tr, tol = to;
   const bool split = (ep.flags & EPF_SPLIT) != 0;
   if (split) {
-    LV_REQUIRE(make_tma_2d_bf16(&trl, ep.res_lo, N, M, (uint64_t)N * 2, 64, 32), LV_ERR_INTERNAL,
+    LV_REQUIRE(make_tma_2d_u8(&trl, ep.res_lo, N, M, (uint64_t)N, 64, 32), LV_ERR_INTERNAL,
                "cuTensorMapEncodeTiled(residual lo) failed");
-    LV_REQUIRE(make_tma_2d_bf16(&tol, ep.out_lo, N, M, (uint64_t)N * 2, 64, 32), LV_ERR_INTERNAL,
+    LV_REQUIRE(make_tma_2d_u8(&tol, ep.out_lo, N, M, (uint64_t)N, 64, 32), LV_ERR_INTERNAL,
                "cuTensorMapEncodeTiled(out lo) failed");
   }
   static bool attr_set = false;
@@ -836,6 +844,9 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<5>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<5>::kSmem));
+    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<6>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PairCfg<6>::kSmem));
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<0>::kSmem));
@@ -857,10 +868,13 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
   const int pairs = std::min(tiles, tc_gemm_num_sms() / 2);
   const int mode = (ep.flags & EPF_SWIGLU) ? 3
                    : !(ep.flags & EPF_RES) ? 0
-                   : split ? 5
+                   : split ? ((K > 1024 || g_split_single) ? 5 : 6)
                    : K <= g_short_k ? 2
                    : (K > 1024 && g_long_k_single) ? 4 : 1;
-  if (mode == 5)
+  if (mode == 6)
+    tc_gemm_pair_kernel<6><<<2 * pairs, kThreads, PairCfg<6>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
+                                                                          M, N, K, ep);
+  else if (mode == 5)
     tc_gemm_pair_kernel<5><<<2 * pairs, kThreads, PairCfg<5>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
                                                                           M, N, K, ep);
   else if (mode == 4)
@@ -884,6 +898,20 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
 }
 
 }  // namespace
+
+bool make_tma_2d_u8(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows,
+                    uint64_t row_stride_bytes, int box_cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)row_stride_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 
 bool make_tma_2d_bf16(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows,
                       uint64_t row_stride_bytes, int box_cols, int box_rows) {

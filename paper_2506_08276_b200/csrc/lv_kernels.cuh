@@ -33,14 +33,16 @@ struct TcGemmPlan;  // cached tensor maps for one (A, W, M, N, K)
 //   v += (res - mean_r) * rstd_r * res_g + res_b     (EPF_RES | EPF_RES_LN)
 //   stats[row][col / 64] = (mean, M2) of the bf16-rounded outputs of each
 //        64-column box (EPF_STATS; combined by ln_stats_finalize)
-//   EPF_SPLIT (with EPF_RES): the residual stream is carried at ~16-bit
-//        mantissa precision as a bf16 pair (hi, lo = bf16(v - hi)): the
-//        residual is res + res_lo, the output is written as out (hi) and
-//        out_lo, and the statistics are taken from the unrounded v. The
-//        consuming GEMMs read hi as their A operand; only the residual adds
-//        and the LayerNorm statistics see the pair. (Rounding the post-LN
-//        residual stream to bf16 at every sublayer was the dominant error of
-//        the bf16 encoder against the fp32 one.)
+//   EPF_SPLIT (with EPF_RES): the residual stream is carried to ~2^-14
+//        absolute precision as hi = bf16(v) plus an int8 correction lo
+//        (lo8_encode: the rounding error in units of 2^-13): the
+//        residual is res + lo8_decode(res_lo), the output is written as out
+//        (hi) and out_lo, and the statistics are taken from the unrounded v.
+//        The consuming GEMMs read hi as their A operand; only the residual
+//        adds and the LayerNorm statistics see the pair. (Rounding the
+//        post-LN residual stream to bf16 at every sublayer was the dominant
+//        error of the bf16 encoder against the fp32 one; the int8 half costs
+//        1 byte per element per read / write.)
 //   out[:, j] = silu(acc[:, g(j)]) * acc[:, u(j)]   (EPF_SWIGLU, alone: weight
 //        rows interleaved per 64 as [gate 64 | up 64]; output width N / 2)
 enum EpiFlag : int {
@@ -55,8 +57,8 @@ struct EpiParams {
   const float *res_g = nullptr;   // [N]  EPF_RES_LN
   const float *res_b = nullptr;   // [N]  EPF_RES_LN
   float2 *stats = nullptr;        // [M][N / 64]  EPF_STATS
-  const __nv_bfloat16 *res_lo = nullptr;  // [M][N]  EPF_SPLIT: low half of the residual
-  __nv_bfloat16 *out_lo = nullptr;        // [M][N]  EPF_SPLIT: low half of the output
+  const int8_t *res_lo = nullptr;  // [M][N]  EPF_SPLIT: int8 correction of the residual
+  int8_t *out_lo = nullptr;        // [M][N]  EPF_SPLIT: int8 correction of the output
   int flags = 0;
 };
 // 2-CTA kernel with the generalised epilogue; needs N % 256 == 0, K % 64 == 0.
@@ -68,11 +70,28 @@ int tc_gemm(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
 int tc_gemm_num_sms();
 // Row-major bf16 [rows][cols] tensor map (row stride in bytes), box
 // (box_cols x box_rows), 128-byte swizzle (box_cols * 2 must be 128).
+// Split residual stream (EPF_SPLIT): v ~= hi + lo8_decode(lo8_encode(v, hi))
+// with hi = bf16(v). The bf16 rounding error v - hi is stored in int8 at a
+// fixed resolution of 2^-13 (|error| <= 127 * 2^-13 covers bf16's half-ulp for
+// |v| < 8, the range of the post-LayerNorm stream); larger values clamp, so a
+// correction is never worse than bf16 alone. Absolute error <= 2^-14.
+constexpr float kLo8Scale = 8192.f;
+__device__ __forceinline__ int lo8_encode(float v, float hi) {
+  const int q = __float2int_rn((v - hi) * kLo8Scale);
+  return max(-127, min(127, q));
+}
+__device__ __forceinline__ float lo8_decode(int q) { return (float)q * (1.f / kLo8Scale); }
+// Row-major int8 [rows][cols] tensor map, box (box_cols x box_rows), 64-byte
+// swizzle (box_cols must be 64): 16-byte chunk j of box row r lands at chunk
+// j ^ ((r >> 1) & 3).
+bool make_tma_2d_u8(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows,
+                    uint64_t row_stride_bytes, int box_cols, int box_rows);
 bool make_tma_2d_bf16(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows,
                       uint64_t row_stride_bytes, int box_cols, int box_rows);
 extern int g_gemm_mode;  // 0 auto (2-CTA pair kernel when N % 256 == 0), 1 force 1-CTA
 extern int g_short_k;    // residual pair GEMMs with K <= g_short_k: 3-buffer epilogue
 extern int g_long_k_single;  // residual pair GEMMs with K > 1024: 1-buffer / 5-stage kernel
+extern int g_split_single;   // split-residual pair GEMMs with K <= 1024: kMode 5 (1 buffer)
 
 // ---- fp32 SIMT GEMM (parity mode, lv_encoder.cu): same contract in fp32.
 cudaError_t f32_gemm(const float *A, const float *W, const float *bias, const float *residual,
