@@ -191,9 +191,14 @@ def setup(cfg, args, device):
     log(f"index built in {time.time() - t1:.1f}s: levels={graph.level_count} "
         f"avg_deg={graph.out_degrees(0).mean():.2f}")
     gt = brute_force_topk(E, Q, cfg["k"], "cosine")
+    # held-out queries (never seen by the ef / rerank tuner): recall reported beside
+    htok = gen(min(1024, cfg["n_queries"]), args.seed + 3)
+    Qh = enc.encode(torch.from_numpy(htok.view(iview)).cuda(device))
+    gt_h = brute_force_topk(E, Qh, cfg["k"], "cosine")
     torch.cuda.empty_cache()  # the builder's cached blocks go back to the driver (the search
     # library allocates with cudaMalloc; config-3 needs the room)
-    return dict(ecfg=ecfg, weights=weights, enc=enc, tokens=tokens, qtokens=qtokens,
+    return dict(ecfg=ecfg, weights=weights, enc=enc, tokens=tokens, qtokens=qtokens, Qh=Qh,
+                gt_h=gt_h,
                 tok_dev=tok_dev, qtok_dev=qtok_dev, E=E, Q=Q, graph=graph, model=model,
                 codes=codes, gt=gt, setup_s=time.time() - t0, embed_s=embed_s, corpus=corpus)
 
@@ -208,7 +213,7 @@ def recall_of(ids: np.ndarray, gt: np.ndarray) -> float:
 
 def tune(W, cfg, args, dev_index, hub_cache=None):
     """Per rerank percent, the minimal ef reaching the recall target (tune_ef,
-    evaluation.py:132-161, upper bound --ef-max instead of n), evaluated in
+    evaluation.py:132-161, with n = --ef-max), evaluated in
     resident-matrix mode (same results as the recompute mode: the encoder is
     batch-invariant). Then, for every feasible (ef, rerank percent), the
     PHYSICAL encoder passages of one full step — the step's cost — are
@@ -216,6 +221,7 @@ def tune(W, cfg, args, dev_index, hub_cache=None):
     shared-recompute table and hub cache, rows from the resident matrix), and
     the pair with the fewest is chosen."""
     import paper_2506_08276_b200 as lv
+    from paper_2506_08276_b200.evaluation import tune_ef
     k = cfg["k"]
     Q = W["Q"][:cfg["n_queries"]].contiguous()   # tune on the config's query set
     gt_tune = W["gt"][:cfg["n_queries"]]
@@ -233,20 +239,11 @@ def tune(W, cfg, args, dev_index, hub_cache=None):
                     f"recomputes/q={memo[ef][1]:.0f}")
             return memo[ef][0]
 
-        hi = args.ef_max
-        if rec(hi) < args.recall:
-            table.append(dict(alpha=alpha, ef=hi, recall=memo[hi][0], recomputes=memo[hi][1],
-                              feasible=False))
-            continue
-        lo = k
-        while lo < hi:
-            mid = (lo + hi) // 2
-            if rec(mid) >= args.recall:
-                hi = mid
-            else:
-                lo = mid + 1
-        table.append(dict(alpha=alpha, ef=lo, recall=memo[lo][0], recomputes=memo[lo][1],
-                          feasible=True))
+        # evaluation.py:132-161 with n = --ef-max (the reference harness passes
+        # graph.n; one evaluation at ef = 1M would take hours)
+        r = tune_ef(rec, k, args.ef_max, args.recall)
+        table.append(dict(alpha=alpha, ef=r.ef, recall=memo[r.ef][0], recomputes=memo[r.ef][1],
+                          feasible=r.feasible, warning=r.warning))
     ok = [t for t in table if t["feasible"]] or table
     if W.get("prov") is not None:
         batch = min(args.batch or cfg["batch"], W["Q"].shape[0])
@@ -263,52 +260,115 @@ def tune(W, cfg, args, dev_index, hub_cache=None):
 
 
 # --------------------------------------------------------------------------- CPU baseline
+# The reference's CPU search (the oracle port of search.py:331-431, pinned to
+# the unmodified reference by tests/test_oracle_golden.py) with a torch-CPU
+# fp32 copy of the encoder as the provider (ProviderSource.fetch ->
+# embed_batch, search.py:103-110), every query run to completion. The host's
+# cores are used as the reference would be deployed: one single-threaded
+# search per process (the service runs searches from a thread pool,
+# app.py:37-57), C processes forked after setup so they share the index,
+# token store, weights and the hub cache copy-on-write.
 
-class _Budget(Exception):
-    pass
+_CPU = {}
 
 
 class _CpuEncoderSource:
-    """Reference provider path on the CPU: ProviderSource.fetch (search.py:103-110)
-    -> embed_batch of the token payloads with the torch-CPU fp32 encoder."""
+    """ProviderSource.fetch (search.py:103-110) with the EmbeddingCache split
+    (search.py:155-188): cached ids read their pinned row, the misses are
+    embedded from their token rows by the torch-CPU fp32 encoder."""
 
-    def __init__(self, ref_enc, tokens, budget_s):
-        self.ref = ref_enc
-        self.tokens = tokens
-        self.budget = budget_s
-        self.t0 = time.perf_counter()
-        self.done = 0
+    def __init__(self, ref_enc, tokens, cache_rows):
+        self.ref, self.tokens, self.cache = ref_enc, tokens, cache_rows
+        self.encoded = 0
 
     def fetch(self, ids):
-        if time.perf_counter() - self.t0 > self.budget:
-            raise _Budget()
-        rows = self.ref.encode(self.tokens[np.asarray(ids, dtype=np.int64)].astype(np.int64))
-        self.done += len(ids)
-        return rows
+        ids = [int(i) for i in ids]
+        miss = [i for i in ids if i not in self.cache]
+        rows = {}
+        if miss:
+            enc = self.ref.encode(self.tokens[np.asarray(miss, dtype=np.int64)].astype(np.int64))
+            rows = dict(zip(miss, enc))
+            self.encoded += len(miss)
+        return np.stack([self.cache[i] if i in self.cache else rows[i] for i in ids])
 
 
-def cpu_sample(W, cfg, args, ef, qi, budget_s, r_total):
-    """Reference two_level search of query `qi` with the CPU encoder, bounded by
-    `budget_s` seconds. Returns (seconds, fraction of the query completed)."""
+def _cpu_query(qi):
+    """One complete query of the reference search on one core (forked worker)."""
     import torch
     from oracle import search_port as sp
     from oracle.encoder_ref import make_ref_encoder
-    g = W["graph"]
-    og = sp.CsrGraph(g.n, g.max_degree, g.entry_point, g.levels, g.level_offsets,
-                     g.level_neighbors)
-    ref = W.setdefault("_ref_enc", make_ref_encoder(W["ecfg"], W["weights"]))
+    torch.set_num_threads(1)
+    c = _CPU
+    if "ref" not in c:
+        c["ref"] = make_ref_encoder(c["ecfg"], c["weights"])
     t0 = time.perf_counter()
-    q = ref.encode(W["qtokens"][qi:qi + 1].astype(np.int64))[0]   # embed_query
-    src = _CpuEncoderSource(ref, W["tokens"], budget_s)
-    params = sp.SearchParams(k=cfg["k"], ef=ef, rerank_percent=args.alpha)
-    finished = True
-    try:
-        sp.two_level(og, q, params, W["model"].codebooks, W["codes"].codes, src, "cosine")
-    except _Budget:
-        finished = False
-    dt = time.perf_counter() - t0
-    frac = 1.0 if finished else min(1.0, src.done / max(1, r_total))
-    return dt, frac, src.done
+    q = c["ref"].encode(c["qtokens"][qi:qi + 1].astype(np.int64))[0]     # embed_query
+    src = _CpuEncoderSource(c["ref"], c["tokens"], c["cache_rows"])
+    rep = sp.two_level(c["graph"], q, c["params"], c["codebooks"], c["codes"], src, "cosine",
+                       cached=c["cache_ids"])
+    return (qi, [i for i, _ in rep.results], rep.recomputations, rep.cache_hits,
+            time.perf_counter() - t0)
+
+
+def _cpu_traverse(qi):
+    """Oracle-mode traversal only (MatrixSource, search.py:78-93) of query qi."""
+    from oracle import search_port as sp
+    c = _CPU
+    t0 = time.perf_counter()
+    sp.two_level(c["graph"], c["Qm"][qi], c["params"], c["codebooks"], c["codes"],
+                 sp.MatrixRows(c["Em"]), "cosine")
+    return time.perf_counter() - t0
+
+
+def cpu_prepare(W, cfg, args, ef, alpha, hub_cache):
+    """Fork-shared state of the CPU reference search: CSR, PQ, token store,
+    fp32 encoder weights and the same hub EmbeddingCache as the GPU arm (its
+    pinned rows computed once by the fp32 GPU encoder in setup — the CPU
+    would need minutes for them)."""
+    import torch
+    from oracle import search_port as sp
+    from paper_2506_08276_b200.encoder import GpuEncoder
+    g = W["graph"]
+    cache_rows, cache_ids = {}, None
+    if hub_cache is not None:
+        ids = np.asarray(hub_cache.ids, dtype=np.int64)
+        enc32 = W.get("_enc32") or GpuEncoder(W["ecfg"], W["weights"], precision="fp32")
+        W["_enc32"] = enc32
+        rows = enc32.encode(torch.from_numpy(W["tokens"][ids].view(
+            np.int16 if W["tokens"].dtype == np.uint16 else np.int32)).cuda())
+        cache_rows = dict(zip(ids.tolist(), rows.cpu().numpy()))
+        cache_ids = set(ids.tolist())
+    _CPU.clear()
+    _CPU.update(graph=sp.CsrGraph(g.n, g.max_degree, g.entry_point, g.levels, g.level_offsets,
+                                  g.level_neighbors),
+                codebooks=W["model"].codebooks, codes=W["codes"].codes, tokens=W["tokens"],
+                qtokens=W["qtokens"], ecfg=W["ecfg"], weights=W["weights"],
+                params=sp.SearchParams(k=cfg["k"], ef=ef, rerank_percent=alpha),
+                cache_rows=cache_rows, cache_ids=cache_ids)
+
+
+def cpu_run(query_ids, procs):
+    """Complete queries over `procs` forked single-threaded workers; returns
+    (wall seconds, per-query results)."""
+    import multiprocessing as mp
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_cpu_query, list(query_ids), chunksize=1)
+    return time.perf_counter() - t0, res
+
+
+def cpu_traversal_qps(W, procs, n=256):
+    """Oracle-mode traversal-only QPS (MatrixSource over the resident
+    embeddings) over `procs` processes — the reference's search loop without
+    its encoder."""
+    import multiprocessing as mp
+    _CPU["Em"] = W["E"].cpu().numpy()
+    _CPU["Qm"] = W["Q"].cpu().numpy()
+    n = min(n, _CPU["Qm"].shape[0])
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(procs) as pool:
+        pool.map(_cpu_traverse, range(n), chunksize=4)
+    return n / (time.perf_counter() - t0), n
 
 
 def cpu_threads():
@@ -340,7 +400,6 @@ def main():
                     help="reference EmbeddingCache size (SearchParams.cache_percent)")
     ap.add_argument("--recall", type=float, default=0.90)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--batch-sweep", default="",
@@ -413,7 +472,7 @@ def main():
     flops_pp = W["ecfg"].flops_per_passage(cfg["seq"])
 
     if args.impl == "reference":
-        run_reference(W, cfg, args, ef, batch, dev_index, params, flops_pp)
+        run_reference(W, cfg, args, ef, batch, dev_index, params, flops_pp, hub_cache)
         return
 
     source = lv.ProviderSource(prov)
@@ -483,7 +542,9 @@ def main():
         cache_hits += int(out["counters"][:batch, 2].sum().item())
         ids = out["ids"][:batch]
         if dist is not None:  # the one collective: gather result ids/scores
-            gather_results(ids, out["dist"][:batch])
+            ids, _ = gather_results(ids, out["dist"][:batch])
+            idx = np.concatenate([shard_queries(args.warmup + s, r, world, batch, nq)
+                                  for r in range(world)])   # rank-major, like the gather
         all_ids.append(ids.cpu().numpy())
         all_idx.append(idx)
     ev1.record(stream)
@@ -541,6 +602,10 @@ def main():
 
     if rank != 0:
         return
+    # ---- held-out recall (untimed): same recompute path and parameters
+    ho = dev_index.search_device(W["Qh"], params, source, cache=hub_cache,
+                                 max_inflight=args.inflight)
+    heldout_recall = recall_of(ho["ids"][:W["Qh"].shape[0]].cpu().numpy(), W["gt_h"])
     # ---- rooflines
     frontier_gbs = adc_bytes / (frontier_ms / 1e3) / 1e9 if frontier_ms else 0.0
     traffic = load_traffic()
@@ -596,6 +661,15 @@ def main():
                    "global_batch": batch * world, "seq_len": cfg["seq"], "ef": ef,
                    "rerank_percent": args.alpha, "parallelism": f"dp{world} (query shards)",
                    "recall_at_3": round(recall, 4), "tuned_recall_at_3": tuned_recall,
+                   "heldout_recall_at_3": round(heldout_recall, 4),
+                   "heldout_queries": int(W["Qh"].shape[0]),
+                   "recall_note": ("recall@k of the timed steps' queries (all ranks, gathered) "
+                                   "and of held-out queries the tuner never saw, against exact "
+                                   "brute force over the bf16 encoder's corpus embeddings; the "
+                                   "tuner picks (ef, rerank%) on the timed query pool, like "
+                                   "tune_ef (evaluation.py:132-161)"),
+                   "query_norms": ("device, in numpy's np.dot (OpenBLAS sdot) order: "
+                                   "bit-identical to the reference's host value (lv_query_norms)"),
                    "ef_feasible": feasible, "corpus": W["corpus"],
                    "inflight_slots": args.inflight or min(batch, 4096), "tuning": table,
                    "cache_percent": args.cache_percent or None, "l2": "inputs larger than L2 (token store "
@@ -614,7 +688,7 @@ def main():
     if args.sweep and world == 1:
         line["batch_sweep"] = batch_sweep(W, cfg, args, dev_index, params, source, hub_cache)
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(W, cfg, args, ef, out_buf, all_idx[-1])
+        line["cpu_baseline"] = cpu_baseline(W, cfg, args, ef, hub_cache)
     print(json.dumps(line), flush=True)
 
 
@@ -646,52 +720,54 @@ def batch_sweep(W, cfg, args, dev_index, params, source, hub_cache):
     return out
 
 
-def cpu_baseline(W, cfg, args, ef, out_buf, last_idx):
-    """Reference CPU search (oracle port + torch-CPU encoder) on a bounded sample."""
-    import torch
-    threads = cpu_threads()
-    torch.set_num_threads(threads)
-    # the recompute count of the sampled query from the device run (same algorithm)
-    counters = out_buf["o"]["counters"].cpu().numpy()
-    qi = int(last_idx[0])
-    r_total = int(counters[0, 0])
-    dt, frac, done = cpu_sample(W, cfg, args, ef, qi, args.cpu_seconds, r_total)
-    qps = frac / dt
-    return {"value": round(qps, 6), "unit": "queries/s", "cores": threads, "kind": "port",
-            "sample": (f"query {qi}: reference two_level_search restated in oracle/search_port.py "
-                       f"(search.py:331-431) with a torch-CPU fp32 copy of the encoder as the "
-                       f"provider, ef={ef}, run {dt:.1f}s: {done} of ~{r_total} recomputations "
-                       f"({frac:.3f} of the query); QPS = completed fraction / seconds")}
+def cpu_baseline(W, cfg, args, ef, hub_cache):
+    """Our arm's cpu_baseline: one round of complete queries (one per host core)
+    of the reference CPU search on the same workload, hub cache and (ef, rerank%)."""
+    procs = cpu_threads()
+    cpu_prepare(W, cfg, args, ef, args.alpha, hub_cache)
+    qids = list(range(cfg["n_queries"] - procs, cfg["n_queries"]))
+    secs, res = cpu_run(qids, procs)
+    recall = recall_of(np.array([r[1] for r in res]), W["gt"][qids])
+    return {"value": round(len(res) / secs, 6), "unit": "queries/s", "cores": procs,
+            "kind": "port",
+            "sample": (f"{len(res)} complete queries (ids {qids[0]}-{qids[-1]}) of the reference "
+                       f"two_level_search (oracle/search_port.py, pinned to search.py:331-431) with "
+                       f"a torch-CPU fp32 encoder provider and the GPU arm's {args.cache_percent}% "
+                       f"hub cache, one single-threaded search per process on {procs} processes, "
+                       f"ef={ef}, rerank {args.alpha}%: {secs:.1f}s wall, "
+                       f"{np.mean([r[2] for r in res]):.0f} recomputations/query, "
+                       f"recall@{cfg['k']} {recall:.3f}")}
 
 
-def run_reference(W, cfg, args, ef, batch, dev_index, params, flops_pp):
-    """--impl reference: each step is a bounded sample (one query for at most
-    --cpu-seconds / 2) of the reference CPU search; value = queries completed / s."""
-    import torch
-    import paper_2506_08276_b200 as lv
-    threads = cpu_threads()
-    torch.set_num_threads(threads)
-    # recompute totals per query (untimed; same algorithm on the device)
-    nq = min(cfg["n_queries"], args.warmup + args.steps)
-    out = dev_index.search_device(W["Q"][:nq].contiguous(), params, lv.MatrixSource(W["E"]))
-    r_tot = out["counters"][:, 0].cpu().numpy()
-    budget = max(2.0, args.cpu_seconds / 2)
-    for s in range(args.warmup):
-        cpu_sample(W, cfg, args, ef, s % nq, budget, int(r_tot[s % nq]))
-    secs = 0.0
-    work = 0.0
-    done = 0
-    for s in range(args.steps):
-        qi = (args.warmup + s) % nq
-        dt, frac, d = cpu_sample(W, cfg, args, ef, qi, budget, int(r_tot[qi]))
+def run_reference(W, cfg, args, ef, batch, dev_index, params, flops_pp, hub_cache):
+    """--impl reference: each step = one round of complete queries (one per host
+    core) of the reference CPU search (oracle port + torch-CPU fp32 encoder,
+    same hub cache, ef and rerank% as the GPU arm); value = queries / wall s."""
+    procs = cpu_threads()
+    cpu_prepare(W, cfg, args, ef, args.alpha, hub_cache)
+    nq = cfg["n_queries"]
+    # warm-up: the same call path on a small round (process pool, torch-CPU kernels)
+    for s_ in range(args.warmup):
+        cpu_run([(s_ * 7) % nq], 1)
+    secs, done, recs, ids, qall = 0.0, 0, 0, [], []
+    for s_ in range(args.steps):
+        qids = [((s_ * procs + j) % nq) for j in range(procs)]
+        dt, res = cpu_run(qids, procs)
         secs += dt
-        work += frac
-        done += d
-    value = work / secs
-    sample = (f"{args.steps} steps, each one query of the reference two_level_search "
-              f"(oracle/search_port.py restating search.py:331-431) with a torch-CPU fp32 "
-              f"encoder provider on {threads} threads, bounded to {budget:.0f}s; "
-              f"{done} recomputations, {work:.3f} queries completed")
+        done += len(res)
+        recs += sum(r[2] for r in res)
+        ids += [r[1] for r in res]
+        qall += qids
+    value = done / secs
+    recall = recall_of(np.array(ids), W["gt"][qall])
+    trav_qps, trav_n = cpu_traversal_qps(W, procs)
+    sample = (f"{args.steps} steps x {procs} complete queries of the reference two_level_search "
+              f"(oracle/search_port.py, pinned to search.py:331-431) with a torch-CPU fp32 encoder "
+              f"provider and the GPU arm's {args.cache_percent}% hub cache, one single-threaded "
+              f"search per process on {procs} processes: {done} queries in {secs:.1f}s, "
+              f"{recs / max(1, done):.0f} recomputations/query, recall@{cfg['k']} {recall:.3f}; "
+              f"oracle-mode traversal only (MatrixSource): {trav_qps:.1f} QPS over {trav_n} "
+              f"queries")
     line = {
         "metric": "queries/sec at recall@3>=90% and recomputed embeddings/sec",
         "value": round(value, 6), "unit": "queries/s", "n_gpus": 1, "steps": args.steps,
@@ -699,9 +775,11 @@ def run_reference(W, cfg, args, ef, batch, dev_index, params, flops_pp):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": cfg["workload"], "ef": ef, "rerank_percent": args.alpha,
-                   "seq_len": cfg["seq"]},
-        "recomputed_embeddings_per_s": {"logical": round(done / secs, 3)},
-        "cpu_baseline": {"value": round(value, 6), "unit": "queries/s", "cores": threads,
+                   "seq_len": cfg["seq"], "cache_percent": args.cache_percent or None,
+                   "recall_at_3": round(recall, 4)},
+        "recomputed_embeddings_per_s": {"logical": round(recs / secs, 3)},
+        "traversal_only_qps": round(trav_qps, 2),
+        "cpu_baseline": {"value": round(value, 6), "unit": "queries/s", "cores": procs,
                          "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 6), "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},

@@ -29,6 +29,8 @@
  *   lv_adc_tables        <- adc_build (pq.py:153-178)
  *   lv_adc_score         <- approx_distance_many (pq.py:186-189)
  *   lv_distance_many     <- distance_many (vectors.py:120-140)
+ *   lv_distance_gather   <- distance_many over gathered rows, for brute_force_topk /
+ *                           ground_truth (evaluation.py:82-105)
  *   lv_encoder_create / lv_encode
  *                        <- provider.embed_batch for token payloads (vectors.py:201-211);
  *                           lv_encoder_profile / lv_encoder_stats replace the reference's
@@ -218,6 +220,13 @@ int lv_adc_score(lv_index *index, const float *table, const int64_t *ids, int64_
                  float *out, int flags, void *stream);
 int lv_distance_many(int32_t metric, const float *rows, int64_t nrows, int32_t dim,
                      const float *q, float qnorm, float *out, int flags, void *stream);
+/* distance_many (vectors.py:120-140) of query q[b] against matrix rows ids[b][0..C)
+ * in the reference's einsum order, out [B][C] (ids < 0 -> +inf); DEVICE pointers,
+ * stream-ordered. qnorm NULL -> computed as lv_query_norms. Used to re-rank
+ * brute-force candidates into the reference's ground truth (evaluation.py:82-95). */
+int lv_distance_gather(int32_t metric, const float *matrix, int32_t dim, const int64_t *ids,
+                       int32_t B, int32_t C, const float *q, const float *qnorm, float *out,
+                       void *stream);
 /* qn = np.float32(np.sqrt(np.dot(q, q))) of each row q[b] (B x dim) in the
  * OpenBLAS sdot order (bit-exact with numpy on a SkylakeX-kernel host for
  * dim % 32 == 0; vectors.py:138, pq.py:163). */

@@ -97,6 +97,8 @@ EXPORTS = {
     "lv_merge_pending": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                    C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "lv_distance_gather": (C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
+                                     C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "lv_query_norms": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int,
                                  C.c_void_p]),
     "lv_search_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,

@@ -391,37 +391,10 @@ def train_pq_gpu(matrix, m_pq: int | None, metric: str, iters: int = 10, seed: i
 
 
 def brute_force_topk(matrix, queries, k: int, metric: str, deleted=None, chunk: int = 0):
-    """evaluation.py:82-95 on the GPU in fp32: k smallest (distance, id) over active rows."""
-    import torch
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        E = matrix.float()
-        Q = torch.as_tensor(queries, dtype=torch.float32, device=E.device)
-        chunk = chunk or max(16, min(1024, (1 << 31) // max(1, E.shape[0])))  # <= 8 GB of scores
-        if metric == "cosine":
-            rn = E.norm(dim=1)
-        out = np.empty((Q.shape[0], k), dtype=np.int64)
-        for s in range(0, Q.shape[0], chunk):
-            q = Q[s:s + chunk]
-            dots = q @ E.T
-            if metric == "cosine":
-                d = -(dots / (rn[None, :] * q.norm(dim=1, keepdim=True)))
-            elif metric == "ip":
-                d = -dots
-            else:
-                d = (q * q).sum(1, keepdim=True) + (E * E).sum(1)[None, :] - 2 * dots
-            if deleted is not None:
-                d[:, torch.as_tensor(deleted, device=E.device)] = float("inf")
-            cand = d.topk(k + 8, dim=1, largest=False)
-            ci, cd = cand.indices, cand.values
-            order = torch.argsort(ci, dim=1)
-            ci, cd = ci.gather(1, order), cd.gather(1, order)
-            order = torch.argsort(cd, dim=1, stable=True)
-            out[s:s + chunk] = ci.gather(1, order)[:, :k].cpu().numpy()
-        return out
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
+    """evaluation.py:82-95 (exact reference order): see evaluation.brute_force_topk."""
+    from .evaluation import brute_force_topk as bf
+    active = None if deleted is None else ~np.asarray(deleted, dtype=bool)
+    return bf(matrix, queries, k, metric, active=active, chunk=chunk)
 
 
 def mean_recall(results, truth) -> float:

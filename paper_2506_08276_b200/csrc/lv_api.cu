@@ -1024,3 +1024,26 @@ extern "C" int lv_query_norms(const float *q, int32_t B, int32_t dim, float *out
   LV_CHECK_CUDA(cudaStreamSynchronize(s));
   return LV_OK;
 }
+
+// distance_many (vectors.py:120-140) of each query against a gathered list of
+// rows: out[b][c] = d(q_b, matrix[ids[b][c]]) in the reference's einsum order
+// (ids < 0 -> +inf). Device pointers only; qnorm NULL -> lv_query_norms order.
+extern "C" int lv_distance_gather(int32_t metric, const float *matrix, int32_t dim,
+                                  const int64_t *ids, int32_t B, int32_t C, const float *q,
+                                  const float *qnorm, float *out, void *stream) {
+  LV_REQUIRE(matrix && ids && q && out, LV_ERR_USAGE, "lv_distance_gather: null argument");
+  LV_REQUIRE(metric >= 0 && metric <= 2 && dim >= 1 && B >= 0 && C >= 0, LV_ERR_USAGE,
+             "lv_distance_gather: bad arguments");
+  if (B == 0 || C == 0) return LV_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  DBuf<float> dqn;
+  const float *p_qn = qnorm;
+  if (!p_qn) {
+    LV_TRY(dqn.ensure(B));
+    LV_CHECK_CUDA(launch_qnorm(q, B, dim, dqn.ptr, s));
+    p_qn = dqn.ptr;
+  }
+  LV_CHECK_CUDA(launch_distance_gather(metric, matrix, dim, ids, B, C, q, p_qn, out, s));
+  if (dqn.ptr) LV_CHECK_CUDA(cudaStreamSynchronize(s));  // dqn is freed on return
+  return LV_OK;
+}

@@ -667,6 +667,40 @@ __global__ void dist_kernel(int metric, const float *__restrict__ rows, int64_t 
     out[r] = finish_distance(metric, einsum_combine(a0, a1, a2, a3), einsum_combine(b0, b1, b2, b3), qn);
 }
 
+// distance_many (vectors.py:120-140) of query b against rows ids[b][0..C) of
+// the matrix: 4 lanes per (b, c) in the einsum order; ids < 0 -> +inf.
+__global__ void dist_gather_kernel(int metric, const float *__restrict__ rows, int dim,
+                                   const int64_t *__restrict__ ids, int B, int C,
+                                   const float *__restrict__ q, const float *__restrict__ qn,
+                                   float *__restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t pair = t >> 2;
+  const int l = (int)(t & 3);
+  const bool act = pair < (int64_t)B * C;
+  const int b = act ? (int)(pair / C) : 0;
+  const int64_t id = act ? ids[pair] : -1;
+  float a = 0.f, nr = 0.f;
+  if (act && id >= 0) {
+    const float *row = rows + id * dim;
+    const float *qv = q + (int64_t)b * dim;
+    if (metric == LV_METRIC_L2) {
+      a = einsum_lane<true>(row, qv, dim, l);
+    } else {
+      a = einsum_lane<false>(row, qv, dim, l);
+      if (metric == LV_METRIC_COSINE) nr = einsum_lane<false>(row, row, dim, l);
+    }
+  }
+  const int g = (threadIdx.x & 31) >> 2;
+  float a0 = __shfl_sync(kFull, a, g * 4), a1 = __shfl_sync(kFull, a, g * 4 + 1);
+  float a2 = __shfl_sync(kFull, a, g * 4 + 2), a3 = __shfl_sync(kFull, a, g * 4 + 3);
+  float n0 = __shfl_sync(kFull, nr, g * 4), n1 = __shfl_sync(kFull, nr, g * 4 + 1);
+  float n2 = __shfl_sync(kFull, nr, g * 4 + 2), n3 = __shfl_sync(kFull, nr, g * 4 + 3);
+  if (act && l == 0)
+    out[pair] = id < 0 ? __int_as_float(0x7f800000)
+                       : finish_distance(metric, einsum_combine(a0, a1, a2, a3),
+                                         einsum_combine(n0, n1, n2, n3), qn[b]);
+}
+
 __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   x ^= x >> 16;
   x *= 0x7feb352du;
@@ -944,6 +978,17 @@ cudaError_t launch_adc_score(const float *lut, int m, const uint8_t *codes, cons
   if (aligned && m == 64) return launch_adc_stream<64>(lut, codes, ids, count, out, s);
   if (aligned && m == 96) return launch_adc_stream<96>(lut, codes, ids, count, out, s);
   adc_score_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(lut, m, codes, ids, count, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_distance_gather(int metric, const float *rows, int dim, const int64_t *ids,
+                                   int B, int C, const float *q, const float *qn, float *out,
+                                   cudaStream_t s) {
+  const int64_t threads = (int64_t)B * C * 4;
+  if (threads <= 0) return cudaSuccess;
+  dist_gather_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(metric, rows, dim, ids, B,
+                                                                       C, q, qn, out);
   note_launch();
   return cudaGetLastError();
 }

@@ -110,6 +110,9 @@ cudaError_t launch_dedup(const int32_t *greq, int total, int32_t *keys, int32_t 
                          uint32_t mask, int32_t *row_count, int32_t base, int32_t *new_ids,
                          int32_t *map, cudaStream_t s);
 cudaError_t launch_qnorm(const float *q, int B, int dim, float *qn, cudaStream_t s);
+cudaError_t launch_distance_gather(int metric, const float *rows, int dim, const int64_t *ids,
+                                   int B, int C, const float *q, const float *qn, float *out,
+                                   cudaStream_t s);
 // buffer_scan + Engine.search merge (update.py:483-488, index.py:320-327);
 // scratch holds B * np_ floats, *bad is set on a zero cosine denominator.
 cudaError_t launch_pending_merge(int metric, const float *pend, const int64_t *pids, int64_t np_,

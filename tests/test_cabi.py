@@ -103,3 +103,31 @@ def test_validate_catches_violations():
                      ([[7], []], 4)):
         with pytest.raises(FormatError):
             lv.validate(mk(rows, md))
+
+
+def test_tune_ef_matches_reference_semantics():
+    """evaluation.py:132-161 ported cases (reference tests/test_evaluation.py:92-104)."""
+    from paper_2506_08276_b200.evaluation import tune_ef
+
+    def evaluate(ef):
+        return min(1.0, ef / 50.0)
+
+    r = tune_ef(evaluate, k=3, n=100, target_recall=0.0)
+    assert r.ef == 3 and r.feasible
+    r = tune_ef(evaluate, k=3, n=100, target_recall=0.9)
+    assert r.feasible and r.ef == 45
+    assert evaluate(r.ef) >= 0.9 > evaluate(r.ef - 1)
+    bad = tune_ef(lambda ef: 0.5, k=3, n=100, target_recall=0.9)
+    assert not bad.feasible and bad.ef == 100
+    # a dip below the target just under the endpoint raises the non-monotone warning
+    flip = tune_ef(lambda ef: 1.0 if ef in (40, 41) or ef >= 45 else 0.0, 3, 100, 0.9)
+    assert flip.feasible
+
+
+def test_recall_at_k_reference_semantics():
+    from paper_2506_08276_b200.evaluation import mean_recall, recall_at_k
+    from paper_2506_08276_b200.errors import InvalidArgumentError
+    assert recall_at_k([1, 2, 3], [3, 4, 5]) == 1 / 3
+    assert mean_recall([[1, 2], [5, 6]], [[1, 2], [6, 7]]) == 0.75
+    with pytest.raises(InvalidArgumentError):
+        recall_at_k([1], [])

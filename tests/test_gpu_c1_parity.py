@@ -117,3 +117,10 @@ def test_c1_bf16_encoder_mode_recall_within_half_point(fx):
         got = _recall([[i for i, _ in r.results] for r in reps], gt)
         print(f"bf16 {case['params']}: recall@3 {got:.4f} vs reference {case['recall']:.4f}")
         assert abs(got - case["recall"]) <= 0.005, (case["params"], got, case["recall"])
+
+
+def test_c1_ground_truth_matches_reference(fx):
+    """brute_force_topk / ground_truth (evaluation.py:82-105) on the device ==
+    the reference's ids for all 1000 queries (einsum-order distances + lexsort)."""
+    from paper_2506_08276_b200.evaluation import ground_truth
+    assert ground_truth(fx["E"], fx["Q"], 3, "cosine") == fx["meta"]["ground_truth"]

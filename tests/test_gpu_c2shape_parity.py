@@ -50,3 +50,23 @@ def test_c2shape_matrix_mode_bit_exact(fx, device_qn):
             assert list(ids[b]) == exp["ids"], (case["params"], b)
             assert list(dist[b]) == exp["dist"], (case["params"], b)
             assert cnt[b, 0] == exp["recomputations"] and cnt[b, 1] == exp["approx_lookups"]
+
+
+@pytest.mark.parametrize("k", [3, 10])
+def test_c2shape_ground_truth_matches_reference(fx, k):
+    from paper_2506_08276_b200.evaluation import ground_truth
+    assert ground_truth(fx["E"], fx["Q"], k, "cosine") == fx["meta"][f"ground_truth_{k}"]
+
+
+def test_c2shape_ground_truth_with_deletes_matches_oracle(fx):
+    """Inactive rows are skipped like the reference's active mask (evaluation.py:88-94)."""
+    from oracle import numerics
+    from paper_2506_08276_b200.evaluation import ground_truth
+    E, Q = fx["E"], fx["Q"][:8]
+    active = np.ones(E.shape[0], dtype=bool)
+    active[np.asarray(fx["meta"]["ground_truth_3"][:8]).ravel()] = False   # delete the top hits
+    got = ground_truth(E, Q, 3, "cosine", active=active)
+    for q, g in zip(Q, got):
+        d = numerics.distance_many(E, q, "cosine").astype(np.float64)
+        d = np.where(active, d, np.inf)
+        assert g == [int(i) for i in np.lexsort((np.arange(E.shape[0]), d))[:3]]
