@@ -292,12 +292,12 @@ class _CpuEncoderSource:
         return np.stack([self.cache[i] if i in self.cache else rows[i] for i in ids])
 
 
-def _cpu_query(qi):
-    """One complete query of the reference search on one core (forked worker)."""
+def _cpu_query(qi, threads=1):
+    """One complete query of the reference search (forked worker: one core)."""
     import torch
     from oracle import search_port as sp
     from oracle.encoder_ref import make_ref_encoder
-    torch.set_num_threads(1)
+    torch.set_num_threads(threads)
     c = _CPU
     if "ref" not in c:
         c["ref"] = make_ref_encoder(c["ecfg"], c["weights"])
@@ -348,12 +348,16 @@ def cpu_prepare(W, cfg, args, ef, alpha, hub_cache):
 
 
 def cpu_run(query_ids, procs):
-    """Complete queries over `procs` forked single-threaded workers; returns
-    (wall seconds, per-query results)."""
+    """Complete queries: procs == 1 runs them in this process with every host
+    thread (torch intra-op); procs > 1 over forked single-threaded workers.
+    Returns (wall seconds, per-query results)."""
     import multiprocessing as mp
     t0 = time.perf_counter()
-    with mp.get_context("fork").Pool(procs) as pool:
-        res = pool.map(_cpu_query, list(query_ids), chunksize=1)
+    if procs == 1:
+        res = [_cpu_query(q, cpu_threads()) for q in query_ids]
+    else:
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_cpu_query, list(query_ids), chunksize=1)
     return time.perf_counter() - t0, res
 
 
@@ -401,6 +405,9 @@ def main():
     ap.add_argument("--recall", type=float, default=0.90)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-procs", type=int, default=0,
+                    help="CPU reference: P single-threaded searches per step in P forked "
+                         "processes (default: one query per step on all host threads)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--batch-sweep", default="",
                     help="also time one step at each of these concurrent-query counts "
@@ -720,38 +727,55 @@ def batch_sweep(W, cfg, args, dev_index, params, source, hub_cache):
     return out
 
 
+def _cpu_mode(args):
+    """(processes, queries per step): default one complete query per step on
+    all host threads (bounded wall time: ~30 s at config-2); --cpu-procs P runs
+    P single-threaded searches per step in P forked processes (the throughput
+    configuration, minutes per step at config-2)."""
+    procs = args.cpu_procs if args.cpu_procs > 0 else 1
+    return procs, procs
+
+
 def cpu_baseline(W, cfg, args, ef, hub_cache):
-    """Our arm's cpu_baseline: one round of complete queries (one per host core)
-    of the reference CPU search on the same workload, hub cache and (ef, rerank%)."""
-    procs = cpu_threads()
+    """Our arm's cpu_baseline: complete queries of the reference CPU search on
+    the same workload, hub cache and (ef, rerank%)."""
+    procs, per = _cpu_mode(args)
     cpu_prepare(W, cfg, args, ef, args.alpha, hub_cache)
-    qids = list(range(cfg["n_queries"] - procs, cfg["n_queries"]))
+    qids = list(range(cfg["n_queries"] - per, cfg["n_queries"]))
     secs, res = cpu_run(qids, procs)
     recall = recall_of(np.array([r[1] for r in res]), W["gt"][qids])
-    return {"value": round(len(res) / secs, 6), "unit": "queries/s", "cores": procs,
+    cores = cpu_threads()
+    how = (f"one process with {cores} torch threads" if procs == 1 else
+           f"one single-threaded search per process on {procs} processes")
+    return {"value": round(len(res) / secs, 6), "unit": "queries/s", "cores": cores,
             "kind": "port",
-            "sample": (f"{len(res)} complete queries (ids {qids[0]}-{qids[-1]}) of the reference "
-                       f"two_level_search (oracle/search_port.py, pinned to search.py:331-431) with "
-                       f"a torch-CPU fp32 encoder provider and the GPU arm's {args.cache_percent}% "
-                       f"hub cache, one single-threaded search per process on {procs} processes, "
-                       f"ef={ef}, rerank {args.alpha}%: {secs:.1f}s wall, "
+            "sample": (f"{len(res)} complete quer{'y' if len(res) == 1 else 'ies'} "
+                       f"(ids {qids[0]}-{qids[-1]}) of the reference two_level_search "
+                       f"(oracle/search_port.py, pinned to search.py:331-431) with a torch-CPU "
+                       f"fp32 encoder provider and the GPU arm's {args.cache_percent}% hub cache, "
+                       f"{how}, ef={ef}, rerank {args.alpha}%: {secs:.1f}s wall, "
                        f"{np.mean([r[2] for r in res]):.0f} recomputations/query, "
                        f"recall@{cfg['k']} {recall:.3f}")}
 
 
 def run_reference(W, cfg, args, ef, batch, dev_index, params, flops_pp, hub_cache):
-    """--impl reference: each step = one round of complete queries (one per host
-    core) of the reference CPU search (oracle port + torch-CPU fp32 encoder,
-    same hub cache, ef and rerank% as the GPU arm); value = queries / wall s."""
-    procs = cpu_threads()
+    """--impl reference: each step = complete queries of the reference CPU
+    search (oracle port + torch-CPU fp32 encoder, same hub cache, ef and
+    rerank% as the GPU arm); value = queries / wall s (see _cpu_mode)."""
+    import torch
+    from oracle.encoder_ref import make_ref_encoder
+    procs, per = _cpu_mode(args)
+    cores = cpu_threads()
     cpu_prepare(W, cfg, args, ef, args.alpha, hub_cache)
     nq = cfg["n_queries"]
-    # warm-up: the same call path on a small round (process pool, torch-CPU kernels)
-    for s_ in range(args.warmup):
-        cpu_run([(s_ * 7) % nq], 1)
+    # warm-up: the provider's CPU kernels on one step-sized batch of passages
+    torch.set_num_threads(cores)
+    ref = _CPU.setdefault("ref", make_ref_encoder(_CPU["ecfg"], _CPU["weights"]))
+    for _ in range(args.warmup):
+        ref.encode(W["tokens"][:8].astype(np.int64))
     secs, done, recs, ids, qall = 0.0, 0, 0, [], []
     for s_ in range(args.steps):
-        qids = [((s_ * procs + j) % nq) for j in range(procs)]
+        qids = [((s_ * per + j) % nq) for j in range(per)]
         dt, res = cpu_run(qids, procs)
         secs += dt
         done += len(res)
@@ -760,14 +784,16 @@ def run_reference(W, cfg, args, ef, batch, dev_index, params, flops_pp, hub_cach
         qall += qids
     value = done / secs
     recall = recall_of(np.array(ids), W["gt"][qall])
-    trav_qps, trav_n = cpu_traversal_qps(W, procs)
-    sample = (f"{args.steps} steps x {procs} complete queries of the reference two_level_search "
-              f"(oracle/search_port.py, pinned to search.py:331-431) with a torch-CPU fp32 encoder "
-              f"provider and the GPU arm's {args.cache_percent}% hub cache, one single-threaded "
-              f"search per process on {procs} processes: {done} queries in {secs:.1f}s, "
+    trav_qps, trav_n = cpu_traversal_qps(W, cores)
+    how = (f"one process with {cores} torch threads" if procs == 1 else
+           f"one single-threaded search per process on {procs} processes")
+    sample = (f"{args.steps} steps x {per} complete quer{'y' if per == 1 else 'ies'} of the "
+              f"reference two_level_search (oracle/search_port.py, pinned to search.py:331-431) "
+              f"with a torch-CPU fp32 encoder provider and the GPU arm's {args.cache_percent}% "
+              f"hub cache, {how}: {done} queries in {secs:.1f}s, "
               f"{recs / max(1, done):.0f} recomputations/query, recall@{cfg['k']} {recall:.3f}; "
-              f"oracle-mode traversal only (MatrixSource): {trav_qps:.1f} QPS over {trav_n} "
-              f"queries")
+              f"oracle-mode traversal only (MatrixSource, {cores} processes): {trav_qps:.1f} QPS "
+              f"over {trav_n} queries")
     line = {
         "metric": "queries/sec at recall@3>=90% and recomputed embeddings/sec",
         "value": round(value, 6), "unit": "queries/s", "n_gpus": 1, "steps": args.steps,
@@ -779,7 +805,7 @@ def run_reference(W, cfg, args, ef, batch, dev_index, params, flops_pp, hub_cach
                    "recall_at_3": round(recall, 4)},
         "recomputed_embeddings_per_s": {"logical": round(recs / secs, 3)},
         "traversal_only_qps": round(trav_qps, 2),
-        "cpu_baseline": {"value": round(value, 6), "unit": "queries/s", "cores": procs,
+        "cpu_baseline": {"value": round(value, 6), "unit": "queries/s", "cores": cores,
                          "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 6), "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},

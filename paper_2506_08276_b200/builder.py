@@ -379,15 +379,39 @@ def train_pq_gpu(matrix, m_pq: int | None, metric: str, iters: int = 10, seed: i
         cnt.scatter_add_(1, assign, torch.ones_like(assign, dtype=torch.float64))
         upd = (sums / cnt.clamp_min(1)[:, :, None]).float()
         cbs = torch.where(cnt[:, :, None] > 0, upd, cbs)
-    codes = torch.empty((n, m_pq), dtype=torch.uint8, device=x.device)
-    cn = (cbs * cbs).sum(-1)
-    for s0 in range(0, n, 65536):
-        blk = x[s0:s0 + 65536].view(-1, m_pq, sub).transpose(0, 1)
-        d = cn[:, None, :] - 2.0 * torch.bmm(blk, cbs.transpose(1, 2))
-        codes[s0:s0 + 65536] = torch.argmin(d, dim=2).transpose(0, 1).to(torch.uint8)
     model = PQModel(dim=dim, padded_dim=padded, m_pq=m_pq, metric=metric,
                     codebooks=cbs.cpu().numpy().astype(np.float32))
-    return model, PQCodes(codes=codes.cpu().numpy())
+    return model, encode_pq_gpu(model, matrix)
+
+
+def encode_pq_gpu(model: PQModel, matrix) -> PQCodes:
+    """pq_encode (pq.py:114-136) on the GPU: per subspace the centroid minimising
+    ||c||^2 - 2 x.c (fp32, tf32 off), lowest index on ties (argmin). The
+    reference computes x.c with a BLAS sgemm whose summation order is the
+    host's; codes agree except where two centroids tie to ~1e-6
+    (tests/test_gpu_builder_parity.py)."""
+    import torch
+    x_in = matrix if hasattr(matrix, "data_ptr") else torch.from_numpy(
+        np.ascontiguousarray(matrix, dtype=np.float32)).cuda()
+    n, dim = x_in.shape
+    m_pq, padded = model.m_pq, model.padded_dim
+    sub = padded // m_pq
+    cbs = torch.from_numpy(np.ascontiguousarray(model.codebooks, dtype=np.float32)).to(x_in.device)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        codes = torch.empty((n, m_pq), dtype=torch.uint8, device=x_in.device)
+        cn = (cbs * cbs).sum(-1)
+        for s0 in range(0, n, 65536):
+            blk = torch.zeros((min(65536, n - s0), padded), dtype=torch.float32,
+                              device=x_in.device)
+            blk[:, :dim] = x_in[s0:s0 + 65536].float()
+            blk = blk.view(-1, m_pq, sub).transpose(0, 1)
+            d = cn[:, None, :] - 2.0 * torch.bmm(blk, cbs.transpose(1, 2))
+            codes[s0:s0 + 65536] = torch.argmin(d, dim=2).transpose(0, 1).to(torch.uint8)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return PQCodes(codes=codes.cpu().numpy())
 
 
 def brute_force_topk(matrix, queries, k: int, metric: str, deleted=None, chunk: int = 0):
