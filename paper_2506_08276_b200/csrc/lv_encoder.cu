@@ -98,7 +98,8 @@ __global__ void embed_ln_kernel(const void *__restrict__ tokens, int token_bytes
       const float val = (v[i] - mean) * rstd * __ldg(g + c) + __ldg(b + c);
       const T hi = from_f<T>(val);
       o[c] = hi;
-      if (out_lo) out_lo[row * d + c] = (int8_t)lo8_encode(val, to_f<T>(hi));  // split stream
+      if (out_lo)  // split stream: offset-binary correction byte (lv_kernels.cuh)
+        out_lo[row * d + c] = (int8_t)((lo8_s8((val - to_f<T>(hi)) * kLo8Scale) & 0xff) ^ 0x80);
     }
 }
 
@@ -300,14 +301,15 @@ __global__ void __launch_bounds__(128) pool_ln_kernel(const __nv_bfloat16 *__res
     for (int p = 0; p < S; ++p) {
       const uint4 u = __ldg(base + (size_t)p * stride);
       const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
-      uint2 ul = make_uint2(0u, 0u);
+      uint2 ul = make_uint2(0x80808080u, 0x80808080u);   // offset-binary zero corrections
       if (base_lo) ul = __ldg(base_lo + (size_t)p * stride);  // split residual: y = hi + lo
-      const int8_t *q = reinterpret_cast<const int8_t *>(&ul);
       const float mu = sst[p].x, rs = sst[p].y;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 f = __bfloat1622float2(h[e]);
-        const float y0 = f.x + lo8_decode(q[2 * e]), y1 = f.y + lo8_decode(q[2 * e + 1]);
+        const uint32_t w = e < 2 ? ul.x : ul.y;
+        const float y0 = fmaf(lo8_get(w, (2 * e) & 3), kLo8Inv, f.x);
+        const float y1 = fmaf(lo8_get(w, (2 * e + 1) & 3), kLo8Inv, f.y);
         acc[2 * e] = fmaf(y0 - mu, rs, acc[2 * e]);
         acc[2 * e + 1] = fmaf(y1 - mu, rs, acc[2 * e + 1]);
       }

@@ -700,10 +700,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               rv[2 * e] = f.x;
               rv[2 * e + 1] = f.y;
             }
-            if constexpr (kSplit) {  // residual = hi + lo
-              const int8_t *q = reinterpret_cast<const int8_t *>(&lo_in) + 8 * (c & 1);
+            if constexpr (kSplit) {  // residual = hi + lo * 2^-13
+              const uint32_t w0 = (c & 1) ? lo_in.z : lo_in.x, w1 = (c & 1) ? lo_in.w : lo_in.y;
 #pragma unroll
-              for (int e = 0; e < 8; ++e) rv[e] += lo8_decode(q[e]);
+              for (int e = 0; e < 4; ++e) {
+                rv[e] = fmaf(lo8_get(w0, e), kLo8Inv, rv[e]);
+                rv[4 + e] = fmaf(lo8_get(w1, e), kLo8Inv, rv[4 + e]);
+              }
             }
             if (fl & EPF_RES_LN) {
               const float4 *g4 = reinterpret_cast<const float4 *>(cv + 128 + 8 * c);
@@ -724,16 +727,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           o.w = pack_bf16(v[6], v[7]);
           *cp = o;
           if constexpr (kSplit) {  // int8 correction of hi; statistics of the unrounded v
-            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&o);
+            const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+            float hf[8];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(h[e]);
-              const uint32_t q0 = (uint32_t)(lo8_encode(v[2 * e], f.x) & 0xff);
-              const uint32_t q1 = (uint32_t)(lo8_encode(v[2 * e + 1], f.y) & 0xff);
-              lo_out[2 * (c & 1) + (e >> 1)] |= (q0 | (q1 << 8)) << (16 * (e & 1));
+            for (int e = 0; e < 4; ++e) {   // the bf16 values just packed, back as floats
+              hf[2 * e] = __uint_as_float(ow[e] << 16);
+              hf[2 * e + 1] = __uint_as_float(ow[e] & 0xffff0000u);
             }
+            lo_out[2 * (c & 1)] = lo8_pack4(v, hf);
+            lo_out[2 * (c & 1) + 1] = lo8_pack4(v + 4, hf + 4);
             if (c & 1) *cpl = make_uint4(lo_out[0], lo_out[1], lo_out[2], lo_out[3]);
-            if (c & 1) lo_out[0] = lo_out[1] = lo_out[2] = lo_out[3] = 0u;
             if (fl & EPF_STATS) {
 #pragma unroll
               for (int e = 0; e < 8; e += 2) {

@@ -70,17 +70,30 @@ int tc_gemm(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
 int tc_gemm_num_sms();
 // Row-major bf16 [rows][cols] tensor map (row stride in bytes), box
 // (box_cols x box_rows), 128-byte swizzle (box_cols * 2 must be 128).
-// Split residual stream (EPF_SPLIT): v ~= hi + lo8_decode(lo8_encode(v, hi))
-// with hi = bf16(v). The bf16 rounding error v - hi is stored in int8 at a
-// fixed resolution of 2^-13 (|error| <= 127 * 2^-13 covers bf16's half-ulp for
-// |v| < 8, the range of the post-LayerNorm stream); larger values clamp, so a
-// correction is never worse than bf16 alone. Absolute error <= 2^-14.
+// Split residual stream (EPF_SPLIT): v ~= hi + lo * 2^-13 with hi = bf16(v) and
+// lo = the bf16 rounding error in units of 2^-13, saturated to an int8 and
+// stored offset-binary (byte = lo + 128). |lo| <= 127 covers bf16's half-ulp
+// for |v| < 8, the range of the post-LayerNorm stream; larger values
+// saturate, so a correction is never worse than bf16 alone. Absolute error
+// <= 2^-14. Four corrections per 32-bit word (byte k = column k).
 constexpr float kLo8Scale = 8192.f;
-__device__ __forceinline__ int lo8_encode(float v, float hi) {
-  const int q = __float2int_rn((v - hi) * kLo8Scale);
-  return max(-127, min(127, q));
+__device__ __forceinline__ uint32_t lo8_s8(float scaled) {   // round-to-nearest, saturate
+  uint32_t q;
+  asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(q) : "f"(scaled));
+  return q;
 }
-__device__ __forceinline__ float lo8_decode(int q) { return (float)q * (1.f / kLo8Scale); }
+// v[0..3], hi[0..3] -> one word of offset-binary corrections
+__device__ __forceinline__ uint32_t lo8_pack4(const float *v, const float *hi) {
+  const uint32_t q0 = lo8_s8((v[0] - hi[0]) * kLo8Scale), q1 = lo8_s8((v[1] - hi[1]) * kLo8Scale);
+  const uint32_t q2 = lo8_s8((v[2] - hi[2]) * kLo8Scale), q3 = lo8_s8((v[3] - hi[3]) * kLo8Scale);
+  return __byte_perm(__byte_perm(q0, q1, 0x0040), __byte_perm(q2, q3, 0x0040), 0x5410) ^
+         0x80808080u;
+}
+// correction of column k (0..3) of a word, as a float (exact), times 2^-13 by the caller
+__device__ __forceinline__ float lo8_get(uint32_t w, int k) {
+  return __int_as_float(__byte_perm(w, 0x4B00u, 0x5440u | (uint32_t)k)) - 8388736.f;
+}
+constexpr float kLo8Inv = 1.f / kLo8Scale;
 // Row-major int8 [rows][cols] tensor map, box (box_cols x box_rows), 64-byte
 // swizzle (box_cols must be 64): 16-byte chunk j of box row r lands at chunk
 // j ^ ((r >> 1) & 3).
