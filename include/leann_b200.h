@@ -94,6 +94,10 @@ extern "C" {
                                 is batch-invariant); measures a configuration's physical
                                 recompute count cheaply (tuning) */
 
+#define LV_GLOBAL_LUT 8       /* lv_search_params.flags, matrix source: read the ADC lookup
+                                tables from global memory per lookup instead of staging each
+                                query's table in shared memory with one bulk copy (A/B) */
+
 /* per-query status codes written to lv_search_outputs.status */
 #define LV_Q_OK 0
 #define LV_Q_AQ_OVERFLOW 1   /* retried internally with a larger queue; never returned */

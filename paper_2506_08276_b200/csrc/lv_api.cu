@@ -416,7 +416,23 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   const bool two_level = p.mode == LV_MODE_TWO_LEVEL;
   const bool enc_src = p.source == LV_SOURCE_ENCODER || p.source == LV_SOURCE_CALLBACK;
   const bool callback = p.source == LV_SOURCE_CALLBACK;
-  int slots = p.max_inflight > 0 ? p.max_inflight : (enc_src ? 4096 : 148 * 16);
+  // matrix source + two-level: each warp stages its query's LUT in shared memory
+  // (one bulk copy per query; LV_GLOBAL_LUT keeps the per-lookup global reads)
+  const bool lut_smem = !enc_src && two_level && !(p.flags & LV_GLOBAL_LUT) && ix->m > 0;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int auto_slots = enc_src ? 4096 : sms * 16;
+  if (lut_smem) {  // the warps whose LUTs fit on the SMs at once
+    const size_t per = frontier_smem_per_warp_lut(ix->max_degree, 2 * ix->max_degree + 2, ix->m);
+    const int wpb = (int)std::max<size_t>(1, std::min<size_t>(kWarpsPerBlock, (227 * 1024) / per));
+    const int bps = (int)std::max<size_t>(1, (228 * 1024) / (per * wpb + 1024));
+    auto_slots = sms * wpb * bps;
+  }
+  int slots = p.max_inflight > 0 ? p.max_inflight : auto_slots;
   slots = std::max(1, std::min(slots, B));
   const int req_cap = 2 * ix->max_degree + 2;
   int64_t aq_cap = aq_cap_override > 0 ? aq_cap_override
@@ -537,6 +553,8 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   c.visits_cap = visits_cap;
   c.blog = d_blog;
   c.blog_cap = blog_cap;
+  c.lut_smem = lut_smem ? 1 : 0;
+  c.warps_per_block = kWarpsPerBlock;
 
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);

@@ -175,6 +175,13 @@ __device__ __forceinline__ float sdot_openblas(const float *__restrict__ x,
   return dot;
 }
 
+// approx_distance_many's row sum with the LUT in shared memory (plain loads).
+__device__ __forceinline__ float adc_one_shared(const float *lut, const uint8_t *__restrict__ code,
+                                                int m) {
+  auto get = [&](int s) -> double { return (double)lut[s * 256 + __ldg(code + s)]; };
+  return __double2float_rn(pairwise_sum(get, m));
+}
+
 // approx distance of one code row against one LUT (pq.py:186-189).
 __device__ __forceinline__ float adc_one(const float *__restrict__ lut,
                                          const uint8_t *__restrict__ code, int m) {

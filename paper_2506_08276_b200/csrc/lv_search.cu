@@ -24,6 +24,9 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
 __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
 
 __device__ __forceinline__ unsigned long long aq_key(float aw, int32_t w, bool elig) {
@@ -45,6 +48,8 @@ struct SlotPtrs {
 };
 
 struct WarpSmem {
+  const float *lut;            // this query's LUT: shared memory (lut_smem) or global
+  bool lut_shared;
   float *req_d;                // [req_cap] exact distances of the pending request
   int32_t *miss_idx;           // [req_cap] row index in the global request buffer (-1 = cached)
   int32_t *fresh;              // [max_degree]
@@ -361,14 +366,15 @@ __device__ void finish_query(const SearchCtx &c, const SlotPtrs &P, SlotState &S
 __device__ void adc_insert(const SearchCtx &c, const SlotPtrs &P, SlotState &S,
                            const WarpSmem &W, int F) {
   const int lane = lane_id();
-  const float *lut = c.luts + (int64_t)S.qi * c.m * kCentroids;
+  const float *lut = W.lut;
   int n_el = 0;
   for (int base = 0; base < F; base += 32) {
     int j = base + lane;
     bool el = false;
     if (j < F) {
       int32_t w = W.fresh[j];
-      float aw = adc_one(lut, c.codes + (int64_t)w * c.m, c.m);
+      float aw = W.lut_shared ? adc_one_shared(lut, c.codes + (int64_t)w * c.m, c.m)
+                              : adc_one(lut, c.codes + (int64_t)w * c.m, c.m);
       el = !bit_test(P.xbits, w);
       bit_set(P.abits, w);
       W.tmpk[j] = aq_key(aw, w, el);
@@ -529,7 +535,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 frontier_kernel(const __grid_constant__ SearchCtx c) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
-  const int slot = blockIdx.x * kWarpsPerBlock + warp;
+  const int slot = blockIdx.x * (blockDim.x >> 5) + warp;
   if (slot >= c.slots) return;
   // carve this warp's scratch
   const size_t per_warp = frontier_smem_per_warp(c.max_degree, c.req_cap);
@@ -541,8 +547,53 @@ frontier_kernel(const __grid_constant__ SearchCtx c) {
   W.miss_idx = reinterpret_cast<int32_t *>(W.req_d + c.req_cap);
   W.fresh = W.miss_idx + c.req_cap;
 
+  uint64_t *lut_bar = nullptr;
+  uint32_t lut_phase = 0;
+  W.lut_shared = c.lut_smem != 0;
+  if (W.lut_shared) {  // [LUT][mbarrier][scratch] per warp
+    float *lut = reinterpret_cast<float *>(smem_raw + frontier_smem_per_warp_lut(
+                                                          c.max_degree, c.req_cap, c.m) * warp);
+    lut_bar = reinterpret_cast<uint64_t *>(lut + (size_t)c.m * kCentroids);
+    base = reinterpret_cast<unsigned char *>(lut_bar) + 16;
+    W.newk = reinterpret_cast<unsigned long long *>(base);
+    W.tmpk = W.newk + c.max_degree;
+    W.req_d = reinterpret_cast<float *>(W.tmpk + c.max_degree);
+    W.miss_idx = reinterpret_cast<int32_t *>(W.req_d + c.req_cap);
+    W.fresh = W.miss_idx + c.req_cap;
+    W.lut = lut;
+    if (lane_id() == 0)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(lut_bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+  }
+  // this warp's query LUT -> shared memory: one cp.async.bulk (TMA engine)
+  auto stage_lut = [&](int qi) {
+    const uint32_t bytes = (uint32_t)c.m * kCentroids * 4;
+    if (lane_id() == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       smem_addr(lut_bar)),
+                   "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+          "[%3];" ::"r"(smem_addr(W.lut)),
+          "l"(c.luts + (int64_t)qi * c.m * kCentroids), "r"(bytes), "r"(smem_addr(lut_bar))
+          : "memory");
+    }
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(ok)
+          : "r"(smem_addr(lut_bar)), "r"(lut_phase)
+          : "memory");
+    lut_phase ^= 1u;
+    __syncwarp();
+  };
   SlotState S = c.st[slot];
   const SlotPtrs P = slot_ptrs(c, slot);
+  if (!W.lut_shared && S.qi >= 0) W.lut = c.luts + (int64_t)S.qi * c.m * kCentroids;
   if (c.source == LV_SOURCE_ENCODER && S.req_n > 0 &&
       (S.phase == PH_ENTRY || S.phase == PH_DESCENT || S.phase == PH_BASE)) {
     // misses were published by the previous launch; rebuild their indices
@@ -564,6 +615,12 @@ frontier_kernel(const __grid_constant__ SearchCtx c) {
       if (!claim(c, S)) {
         S.phase = PH_FINISHED;
         break;
+      }
+      if (c.mode == LV_MODE_TWO_LEVEL) {
+        if (W.lut_shared)
+          stage_lut(S.qi);
+        else
+          W.lut = c.luts + (int64_t)S.qi * c.m * kCentroids;
       }
     }
     bool emitted = advance(c, P, S, W);
@@ -881,18 +938,27 @@ __global__ void slot_reset_kernel(SlotState *st, int slots) {
 }  // namespace
 
 size_t frontier_smem_bytes(const SearchCtx &c) {
-  return frontier_smem_per_warp(c.max_degree, c.req_cap) * kWarpsPerBlock;
+  return (c.lut_smem ? frontier_smem_per_warp_lut(c.max_degree, c.req_cap, c.m)
+                     : frontier_smem_per_warp(c.max_degree, c.req_cap)) *
+         c.warps_per_block;
 }
 
-cudaError_t launch_frontier(const SearchCtx &ctx, cudaStream_t s) {
+cudaError_t launch_frontier(SearchCtx &ctx, cudaStream_t s) {
+  if (ctx.warps_per_block <= 0) ctx.warps_per_block = kWarpsPerBlock;
+  if (ctx.lut_smem) {  // as many warps per block as their LUTs fit (<= 227 KB)
+    const size_t per = frontier_smem_per_warp_lut(ctx.max_degree, ctx.req_cap, ctx.m);
+    ctx.warps_per_block = (int)std::max<size_t>(1, std::min<size_t>(kWarpsPerBlock,
+                                                                   (227 * 1024) / per));
+  }
   size_t smem = frontier_smem_bytes(ctx);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(frontier_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  int blocks = (ctx.slots + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  frontier_kernel<<<blocks, kWarpsPerBlock * 32, smem, s>>>(ctx);
+  const int wpb = ctx.warps_per_block;
+  int blocks = (ctx.slots + wpb - 1) / wpb;
+  frontier_kernel<<<blocks, wpb * 32, smem, s>>>(ctx);
   note_launch();
   return cudaGetLastError();
 }

@@ -88,11 +88,20 @@ struct SearchCtx {
   int32_t visits_cap;
   int32_t *blog;
   int32_t blog_cap;
+  // LUT staging: 1 = each warp copies its query's LUT into shared memory with
+  // one bulk (TMA-engine) copy when it claims the query (matrix source: a
+  // warp runs its queries to completion, so each LUT crosses HBM once)
+  int32_t lut_smem;
+  int32_t warps_per_block;
 };
 
 __host__ __device__ inline size_t frontier_smem_per_warp(int max_degree, int req_cap) {
   size_t per = (size_t)max_degree * 16 + (size_t)req_cap * 8 + (size_t)max_degree * 4;
   return (per + 15) & ~size_t(15);
+}
+// with the LUT in shared memory: LUT (m x 256 fp32) + its mbarrier + the scratch
+__host__ __device__ inline size_t frontier_smem_per_warp_lut(int max_degree, int req_cap, int m) {
+  return (size_t)m * 256 * 4 + 16 + frontier_smem_per_warp(max_degree, req_cap);
 }
 
 // launchers (lv_search.cu)
@@ -121,7 +130,7 @@ cudaError_t launch_pending_merge(int metric, const float *pend, const int64_t *p
                                  int *bad, cudaStream_t s);
 cudaError_t launch_slot_reset(SlotState *st, int slots, cudaStream_t s);
 cudaError_t launch_count_zero(const float *v, int n, int32_t *count, cudaStream_t s);
-cudaError_t launch_frontier(const SearchCtx &ctx, cudaStream_t s);
+cudaError_t launch_frontier(SearchCtx &ctx, cudaStream_t s);
 size_t frontier_smem_bytes(const SearchCtx &ctx);
 
 }  // namespace lv
