@@ -94,9 +94,10 @@ extern "C" {
                                 is batch-invariant); measures a configuration's physical
                                 recompute count cheaply (tuning) */
 
-#define LV_GLOBAL_LUT 8       /* lv_search_params.flags, matrix source: read the ADC lookup
-                                tables from global memory per lookup instead of staging each
-                                query's table in shared memory with one bulk copy (A/B) */
+#define LV_SMEM_LUT 8         /* lv_search_params.flags, matrix source: stage each query's ADC
+                                lookup table in shared memory with one bulk copy instead of
+                                reading it from global memory per lookup (A/B; slower at
+                                config-2 shape: 64 KiB per warp caps residency at 3 warps/SM) */
 
 /* per-query status codes written to lv_search_outputs.status */
 #define LV_Q_OK 0

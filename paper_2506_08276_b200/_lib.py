@@ -21,7 +21,7 @@ LV_SOURCE_CALLBACK = 2
 LV_IO_DEVICE = 1
 LV_NO_SHARED_RECOMPUTE = 2
 LV_DRY_RECOMPUTE = 4
-LV_GLOBAL_LUT = 8
+LV_SMEM_LUT = 8
 
 
 class IndexDesc(C.Structure):

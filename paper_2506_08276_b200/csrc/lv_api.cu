@@ -416,9 +416,12 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   const bool two_level = p.mode == LV_MODE_TWO_LEVEL;
   const bool enc_src = p.source == LV_SOURCE_ENCODER || p.source == LV_SOURCE_CALLBACK;
   const bool callback = p.source == LV_SOURCE_CALLBACK;
-  // matrix source + two-level: each warp stages its query's LUT in shared memory
-  // (one bulk copy per query; LV_GLOBAL_LUT keeps the per-lookup global reads)
-  const bool lut_smem = !enc_src && two_level && !(p.flags & LV_GLOBAL_LUT) && ix->m > 0;
+  // LV_SMEM_LUT (matrix source, two-level): each warp stages its query's LUT in
+  // shared memory with one bulk copy. Measured 3x slower than the default
+  // per-lookup global reads at config-2 shape (profiles/r02_frontier_lut_ab.txt):
+  // a 64 KiB table per warp leaves 3 warps per SM, and this latency-bound
+  // traversal needs the ~16 warps per SM the small-footprint kernel keeps.
+  const bool lut_smem = !enc_src && two_level && (p.flags & LV_SMEM_LUT) && ix->m > 0;
   int sms = 148;
   {
     int dev = 0;

@@ -70,3 +70,19 @@ def test_c2shape_ground_truth_with_deletes_matches_oracle(fx):
         d = numerics.distance_many(E, q, "cosine").astype(np.float64)
         d = np.where(active, d, np.inf)
         assert g == [int(i) for i in np.lexsort((np.arange(E.shape[0]), d))[:3]]
+
+
+def test_c2shape_smem_lut_path_bit_exact(fx):
+    """LV_SMEM_LUT (each query's table staged in shared memory by one bulk copy)
+    returns the same bits as the default per-lookup path and the reference."""
+    import torch
+    lv = fx["lv"]
+    model, codes = fx["pq"]
+    dev = lv.search.device_index_for(fx["g"], model, codes)
+    case = fx["meta"]["cases"][0]
+    out = dev.search_device(torch.from_numpy(fx["Q"]).cuda(), lv.SearchParams(**case["params"]),
+                            lv.MatrixSource(torch.from_numpy(fx["E"]).cuda()), smem_lut=True)
+    ids = out["ids"].cpu().numpy()
+    dist = out["dist"].cpu().numpy().view(np.uint32)
+    for b, exp in enumerate(case["reports"]):
+        assert list(ids[b]) == exp["ids"] and list(dist[b]) == exp["dist"]

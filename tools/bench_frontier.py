@@ -1,6 +1,6 @@
 """Matrix-source frontier kernel A/B: the query's ADC table staged in shared
-memory by one bulk copy (default) vs read from global memory per lookup
-(LV_GLOBAL_LUT). Config-2-shape index (tests/golden/c2shape: 100k x 768,
+memory by one bulk copy (LV_SMEM_LUT) vs read from global memory per lookup
+(default). Config-2-shape index (tests/golden/c2shape: 100k x 768,
 M=32, PQ m=64), 4096 queries (the 512 fixture queries tiled, perturbed)."""
 import json
 import sys
@@ -26,9 +26,9 @@ for ef in (64, 128):
     p = lv.SearchParams(k=3, ef=ef, rerank_percent=30.0)
     res = {}
     for gl in (False, True):
-        dev.search_device(Qt, p, lv.MatrixSource(Et), global_lut=gl)   # warm
+        dev.search_device(Qt, p, lv.MatrixSource(Et), smem_lut=not gl)   # warm
         torch.cuda.synchronize()
-        r = dev.search_device(Qt, p, lv.MatrixSource(Et), global_lut=gl)
+        r = dev.search_device(Qt, p, lv.MatrixSource(Et), smem_lut=not gl)
         st = dev.last_stats()
         res["global" if gl else "smem"] = (r["ids"].cpu().numpy(), st)
     a, b = res["smem"], res["global"]
