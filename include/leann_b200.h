@@ -99,6 +99,10 @@ extern "C" {
                                 reading it from global memory per lookup (A/B; slower at
                                 config-2 shape: 64 KiB per warp caps residency at 3 warps/SM) */
 
+#define LV_HASH_VISITED 16    /* lv_search_params.flags, two-level: per-query visited sets as
+                                bounded hash sets (2 x AQ capacity) instead of dense n-bit
+                                bitmaps; automatic when the bitmaps would exceed 4 GiB */
+
 /* per-query status codes written to lv_search_outputs.status */
 #define LV_Q_OK 0
 #define LV_Q_AQ_OVERFLOW 1   /* retried internally with a larger queue; never returned */

@@ -22,6 +22,7 @@ LV_IO_DEVICE = 1
 LV_NO_SHARED_RECOMPUTE = 2
 LV_DRY_RECOMPUTE = 4
 LV_SMEM_LUT = 8
+LV_HASH_VISITED = 16
 
 
 class IndexDesc(C.Structure):

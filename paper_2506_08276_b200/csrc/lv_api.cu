@@ -67,6 +67,7 @@ struct Workspace {
   DBuf<uint32_t> eq_id;
   DBuf<unsigned long long> aq;
   DBuf<uint32_t> abits, xbits;
+  DBuf<uint32_t> aset, xset;  // bounded hash sets (hash visited mode)
   DBuf<int32_t> xlist, req, greq;
   DBuf<int32_t> counters;  // [0] greq_total, [1] queue_head, [2] done_count
   DBuf<unsigned long long> bytes;  // frontier algorithmic bytes
@@ -448,12 +449,35 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   LV_TRY(ws.eq_d.ensure((size_t)slots * p.ef));
   LV_TRY(ws.eq_id.ensure((size_t)slots * p.ef));
   LV_TRY(ws.aq.ensure((size_t)slots * (two_level ? aq_cap : 1)));
-  bool fresh_bits = ws.abits.cap < (size_t)slots * words;
-  LV_TRY(ws.abits.ensure((size_t)slots * words));
-  LV_TRY(ws.xbits.ensure((size_t)slots * words));
-  if (fresh_bits || ws.bits_dirty) {  // kept all-zero between queries by finish_query
-    LV_CHECK_CUDA(cudaMemsetAsync(ws.abits.ptr, 0, ws.abits.cap * 4, s));
-    LV_CHECK_CUDA(cudaMemsetAsync(ws.xbits.ptr, 0, ws.xbits.cap * 4, s));
+  // visited sets (approx_known / exact_known): dense bitmaps cost 2 x slots x n/8
+  // bytes (1 GB at config-2 with 4096 slots, 41 GB at 10M nodes with 16k);
+  // above a 4 GiB budget (or with LV_HASH_VISITED) two-level searches use
+  // bounded per-slot hash sets of 2 x aq_cap entries instead (the AQ bounds
+  // approx_known; overflow re-runs use bitmaps with <= 64 slots)
+  const double bitmap_bytes = 2.0 * slots * (double)words * 4;
+  const bool hashed = two_level && aq_cap_override == 0 &&
+                      ((p.flags & LV_HASH_VISITED) || bitmap_bytes > 4.0 * (1ull << 30));
+  uint32_t vmask = 0;
+  if (hashed) {
+    uint64_t cap = 1;
+    while (cap < (uint64_t)(2 * aq_cap + 4096)) cap <<= 1;
+    vmask = (uint32_t)(cap - 1);
+    const size_t need = (size_t)slots * cap;
+    const bool fresh = ws.aset.cap < need;
+    LV_TRY(ws.aset.ensure(need));
+    LV_TRY(ws.xset.ensure(need));
+    if (fresh || ws.bits_dirty) {  // finish_query resets a finished slot's tables
+      LV_CHECK_CUDA(cudaMemsetAsync(ws.aset.ptr, 0xff, ws.aset.cap * 4, s));
+      LV_CHECK_CUDA(cudaMemsetAsync(ws.xset.ptr, 0xff, ws.xset.cap * 4, s));
+    }
+  } else {
+    bool fresh_bits = ws.abits.cap < (size_t)slots * words;
+    LV_TRY(ws.abits.ensure((size_t)slots * words));
+    LV_TRY(ws.xbits.ensure((size_t)slots * words));
+    if (fresh_bits || ws.bits_dirty) {  // kept all-zero between queries by finish_query
+      LV_CHECK_CUDA(cudaMemsetAsync(ws.abits.ptr, 0, ws.abits.cap * 4, s));
+      LV_CHECK_CUDA(cudaMemsetAsync(ws.xbits.ptr, 0, ws.xbits.cap * 4, s));
+    }
   }
   ws.bits_dirty = true;  // cleared below once every query has finished
   LV_TRY(ws.xlist.ensure((size_t)slots * xl_cap));
@@ -537,8 +561,11 @@ int search_pass(lv_index *ix, const float *d_q, const float *d_qn, int B, const 
   c.eq_d = ws.eq_d.ptr;
   c.eq_id = ws.eq_id.ptr;
   c.aq = ws.aq.ptr;
-  c.abits = ws.abits.ptr;
-  c.xbits = ws.xbits.ptr;
+  c.abits = hashed ? nullptr : ws.abits.ptr;
+  c.xbits = hashed ? nullptr : ws.xbits.ptr;
+  c.aset = hashed ? ws.aset.ptr : nullptr;
+  c.xset = hashed ? ws.xset.ptr : nullptr;
+  c.vmask = vmask;
   c.xlist = ws.xlist.ptr;
   c.req = ws.req.ptr;
   c.greq = ws.greq.ptr;

@@ -37,12 +37,56 @@ __device__ __forceinline__ int32_t aq_id(unsigned long long key) {
   return (int32_t)(((uint32_t)key) >> 1);
 }
 
+// A per-query set of node ids: approx_known / exact_known of two_level_search
+// (search.py:364-366). Dense bitmap over [0, n) or a bounded open-addressing
+// hash set (linear probing, keys inserted with atomicCAS; all lanes of a warp
+// may insert distinct ids concurrently).
+struct VSet {
+  uint32_t *bits;   // bitmap mode
+  uint32_t *keys;   // hash mode (mask != 0)
+  uint32_t mask;
+  __device__ __forceinline__ bool test(int32_t w) const {
+    if (!mask) return bit_test(bits, w);
+    uint32_t h = hash_id((uint32_t)w) & mask;
+    while (true) {
+      const uint32_t k = keys[h];
+      if (k == (uint32_t)w) return true;
+      if (k == 0xffffffffu) return false;
+      h = (h + 1) & mask;
+    }
+  }
+  __device__ __forceinline__ void insert(int32_t w) const {
+    if (!mask) {
+      bit_set(bits, w);
+      return;
+    }
+    uint32_t h = hash_id((uint32_t)w) & mask;
+    while (true) {
+      const uint32_t k = keys[h];
+      if (k == (uint32_t)w) return;
+      if (k == 0xffffffffu) {
+        const uint32_t old = atomicCAS(keys + h, 0xffffffffu, (uint32_t)w);
+        if (old == 0xffffffffu || old == (uint32_t)w) return;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+  __device__ static __forceinline__ uint32_t hash_id(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+  }
+};
+
 struct SlotPtrs {
   float *eq_d;
   uint32_t *eq_id;
   unsigned long long *aq;
-  uint32_t *abits;
-  uint32_t *xbits;
+  VSet aset;   // approx_known
+  VSet xset;   // exact_known
   int32_t *xlist;
   int32_t *req;
 };
@@ -62,8 +106,14 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(const SearchCtx &c, int slot) {
   p.eq_d = c.eq_d + (int64_t)slot * c.ef;
   p.eq_id = c.eq_id + (int64_t)slot * c.ef;
   p.aq = c.aq + (int64_t)slot * c.aq_cap;
-  p.abits = c.abits + (int64_t)slot * c.words;
-  p.xbits = c.xbits + (int64_t)slot * c.words;
+  if (c.vmask) {
+    const int64_t cap = (int64_t)c.vmask + 1;
+    p.aset = VSet{nullptr, c.aset + (int64_t)slot * cap, c.vmask};
+    p.xset = VSet{nullptr, c.xset + (int64_t)slot * cap, c.vmask};
+  } else {
+    p.aset = VSet{c.abits + (int64_t)slot * c.words, nullptr, 0u};
+    p.xset = VSet{c.xbits + (int64_t)slot * c.words, nullptr, 0u};
+  }
   p.xlist = c.xlist + (int64_t)slot * c.xl_cap;
   p.req = c.req + (int64_t)slot * c.req_cap;
   return p;
@@ -143,7 +193,7 @@ __device__ int32_t eq_pop(const SlotPtrs &P, SlotState &S) {
 
 // CSR row of v at `level` minus the nodes whose bit is set, in CSR order
 // (graph.py:50-52 + search.py:269 / :314 / :385).
-__device__ int filter_row(const SearchCtx &c, int32_t v, int level, const uint32_t *bits,
+__device__ int filter_row(const SearchCtx &c, int32_t v, int level, const VSet &bits,
                           int32_t *out) {
   const int lane = lane_id();
   const uint64_t *off = c.offs[level];
@@ -157,7 +207,7 @@ __device__ int filter_row(const SearchCtx &c, int32_t v, int level, const uint32
     bool keep = false;
     if (i < deg) {
       w = (int32_t)__ldg(row + i);
-      keep = !bit_test(bits, w);
+      keep = !bits.test(w);
     }
     unsigned bal = __ballot_sync(kFull, keep);
     if (keep) out[cnt + __popc(bal & lanemask_lt())] = w;
@@ -173,7 +223,7 @@ __device__ void xlist_append(const SearchCtx &c, const SlotPtrs &P, SlotState &S
   const int lane = lane_id();
   for (int r = lane; r < cnt; r += 32) {
     int32_t w = ids[r];
-    if (set_bits) bit_set(P.xbits, w);
+    if (set_bits) P.xset.insert(w);
     int pos = S.xl_len + r;
     if (pos < c.xl_cap) P.xlist[pos] = w;
   }
@@ -343,16 +393,25 @@ __device__ void finish_query(const SearchCtx &c, const SlotPtrs &P, SlotState &S
     c.out_counters[(int64_t)S.qi * 4 + 3] = S.expansions;
     if (c.out_status) c.out_status[S.qi] = S.status;
   }
-  // clear the slot's bitmaps: every set bit belongs to an AQ or xlist id
-  for (int i = lane; i < S.aq_len; i += 32) {
-    int32_t w = aq_id(P.aq[i]);
-    P.abits[w >> 5] = 0u;
-    P.xbits[w >> 5] = 0u;
-  }
-  if (S.xl_len <= c.xl_cap) {
-    for (int i = lane; i < S.xl_len; i += 32) P.xbits[P.xlist[i] >> 5] = 0u;
-  } else {
-    for (int64_t i = lane; i < c.words; i += 32) P.xbits[i] = 0u;
+  if (c.vmask) {  // hash sets: reset both tables (16-byte stores, whole warp)
+    const int64_t n4 = ((int64_t)c.vmask + 1) / 4;
+    uint4 *a4 = reinterpret_cast<uint4 *>(P.aset.keys), *x4 = reinterpret_cast<uint4 *>(P.xset.keys);
+    const uint4 e = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    for (int64_t i = lane; i < n4; i += 32) {
+      a4[i] = e;
+      x4[i] = e;
+    }
+  } else {  // clear the slot's bitmaps: every set bit belongs to an AQ or xlist id
+    for (int i = lane; i < S.aq_len; i += 32) {
+      int32_t w = aq_id(P.aq[i]);
+      P.aset.bits[w >> 5] = 0u;
+      P.xset.bits[w >> 5] = 0u;
+    }
+    if (S.xl_len <= c.xl_cap) {
+      for (int i = lane; i < S.xl_len; i += 32) P.xset.bits[P.xlist[i] >> 5] = 0u;
+    } else {
+      for (int64_t i = lane; i < c.words; i += 32) P.xset.bits[i] = 0u;
+    }
   }
   __syncwarp();
   if (lane == 0) atomicAdd(c.done_count, 1);
@@ -375,8 +434,8 @@ __device__ void adc_insert(const SearchCtx &c, const SlotPtrs &P, SlotState &S,
       int32_t w = W.fresh[j];
       float aw = W.lut_shared ? adc_one_shared(lut, c.codes + (int64_t)w * c.m, c.m)
                               : adc_one(lut, c.codes + (int64_t)w * c.m, c.m);
-      el = !bit_test(P.xbits, w);
-      bit_set(P.abits, w);
+      el = !P.xset.test(w);
+      P.aset.insert(w);
       W.tmpk[j] = aq_key(aw, w, el);
     }
     n_el += __popc(__ballot_sync(kFull, el));
@@ -471,7 +530,7 @@ __device__ bool advance(const SearchCtx &c, const SlotPtrs &P, SlotState &S, con
         S.phase = PH_BASE;
         continue;
       }
-      int cnt = filter_row(c, S.cur, S.level, P.xbits, P.req);
+      int cnt = filter_row(c, S.cur, S.level, P.xset, P.req);
       S.bytes += 16 + 4 * (long long)(c.offs[S.level][S.cur + 1] - c.offs[S.level][S.cur]);
       if (cnt == 0) {
         S.level -= 1;
@@ -493,14 +552,14 @@ __device__ bool advance(const SearchCtx &c, const SlotPtrs &P, SlotState &S, con
     S.expansions += 1;
     S.bytes += 16 + 4 * (long long)(c.offs[0][u + 1] - c.offs[0][u]);
     if (c.mode == LV_MODE_EXACT_BESTFIRST) {
-      int cnt = filter_row(c, u, 0, P.xbits, P.req);
+      int cnt = filter_row(c, u, 0, P.xset, P.req);
       if (cnt == 0) continue;
       xlist_append(c, P, S, P.req, cnt, true);  // claimed (search.py:317-318)
       S.req_n = cnt;
       emit(c, P, S, W);
       return true;
     }
-    int F = filter_row(c, u, 0, P.abits, W.fresh);
+    int F = filter_row(c, u, 0, P.aset, W.fresh);
     if (F > 0) {
       if (S.aq_len + F > c.aq_cap) {
         S.status = LV_Q_AQ_OVERFLOW;

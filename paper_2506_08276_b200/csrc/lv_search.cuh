@@ -68,7 +68,12 @@ struct SearchCtx {
   float *eq_d;
   uint32_t *eq_id;
   unsigned long long *aq;
-  uint32_t *abits, *xbits;
+  uint32_t *abits, *xbits;   // dense per-slot bitmaps [slots][words] (vmask == 0)
+  // bounded per-slot open-addressing sets [slots][vmask + 1] of node ids
+  // (0xffffffff = empty), used instead of the bitmaps when vmask != 0: memory
+  // O(slots x aq_cap) instead of O(slots x n) (config-3/5: 16k slots x 10M nodes)
+  uint32_t *aset, *xset;
+  uint32_t vmask;
   int32_t *xlist;
   int32_t *req;
   // global request buffer (encoder source)

@@ -522,7 +522,7 @@ class DeviceIndex:
     def search_device(self, Q, params: SearchParams, source, qn=None,
                       cache: EmbeddingCache | None = None, max_inflight: int = 0,
                       out: dict | None = None, shared_recompute: bool = True,
-                      dry_matrix=None, smem_lut: bool = False):
+                      dry_matrix=None, smem_lut: bool = False, hash_visited: bool = False):
         """Device-resident batch search: ``Q`` is a CUDA float32 tensor [B, dim],
         ``qn`` a CUDA tensor [B] or None (norms then computed on the device).
         Returns CUDA tensors ids [B, k] (int64, -1 padded), dist [B, k],
@@ -544,7 +544,8 @@ class DeviceIndex:
         p.mode = _lib.LV_MODE[params.mode]
         p.max_inflight = max_inflight
         p.flags = (_lib.LV_IO_DEVICE | (0 if shared_recompute else _lib.LV_NO_SHARED_RECOMPUTE)
-                   | (_lib.LV_SMEM_LUT if smem_lut else 0))
+                   | (_lib.LV_SMEM_LUT if smem_lut else 0)
+                   | (_lib.LV_HASH_VISITED if hash_visited else 0))
         kind = self._bind_source(source, p, dry_matrix)
         self.set_cache(cache, kind, source)
         p.use_cache = 1 if cache is not None else 0

@@ -86,3 +86,25 @@ def test_c2shape_smem_lut_path_bit_exact(fx):
     dist = out["dist"].cpu().numpy().view(np.uint32)
     for b, exp in enumerate(case["reports"]):
         assert list(ids[b]) == exp["ids"] and list(dist[b]) == exp["dist"]
+
+
+def test_c2shape_hash_visited_sets_bit_exact(fx):
+    """LV_HASH_VISITED (bounded per-query hash sets instead of n-bit bitmaps —
+    the automatic choice at 10M nodes x 16k queries) returns the reference's
+    bits, in matrix mode and across repeated calls (tables reset per query)."""
+    import torch
+    lv = fx["lv"]
+    model, codes = fx["pq"]
+    dev = lv.search.device_index_for(fx["g"], model, codes)
+    for _ in range(2):
+        for case in fx["meta"]["cases"]:
+            out = dev.search_device(torch.from_numpy(fx["Q"]).cuda(),
+                                    lv.SearchParams(**case["params"]),
+                                    lv.MatrixSource(torch.from_numpy(fx["E"]).cuda()),
+                                    hash_visited=True, max_inflight=64)
+            ids = out["ids"].cpu().numpy()
+            dist = out["dist"].cpu().numpy().view(np.uint32)
+            cnt = out["counters"].cpu().numpy()
+            for b, exp in enumerate(case["reports"]):
+                assert list(ids[b]) == exp["ids"] and list(dist[b]) == exp["dist"]
+                assert cnt[b, 0] == exp["recomputations"]

@@ -158,3 +158,22 @@ def test_shared_recompute_is_transparent(world):
         assert x.approx_lookups == y.approx_lookups
     assert phys_a == sum(x.recomputations for x in a)
     assert phys_b < phys_a
+
+
+def test_hash_visited_recompute_mode_matches_bitmaps(world):
+    """Recompute (encoder) source with bounded hash visited sets == bitmaps."""
+    import torch
+    lv = world["lv"]
+    from paper_2506_08276_b200.encoder import EncoderProvider
+    w = world["bf16"]
+    g = lv.load_graph(w["dir"] / "graph.bin")
+    model, codes = lv.load_pq(w["dir"] / "pq.bin")
+    dev = lv.search.device_index_for(g, model, codes)
+    src = lv.ProviderSource(EncoderProvider(w["enc"], w["store"]))
+    Q = torch.from_numpy(w["Q"]).cuda()
+    p = lv.SearchParams(k=3, ef=48, rerank_percent=30.0)
+    a = dev.search_device(Q, p, src)
+    a = {k: v.clone() for k, v in a.items()}
+    b = dev.search_device(Q, p, src, hash_visited=True)
+    assert torch.equal(a["ids"], b["ids"]) and torch.equal(a["dist"], b["dist"])
+    assert torch.equal(a["counters"], b["counters"])

@@ -25,14 +25,15 @@ out = {}
 for ef in (64, 128):
     p = lv.SearchParams(k=3, ef=ef, rerank_percent=30.0)
     res = {}
-    for gl in (False, True):
-        dev.search_device(Qt, p, lv.MatrixSource(Et), smem_lut=not gl)   # warm
+    for name, kw in (("smem", dict(smem_lut=True)), ("global", {}),
+                     ("hashset", dict(hash_visited=True))):
+        dev.search_device(Qt, p, lv.MatrixSource(Et), **kw)   # warm
         torch.cuda.synchronize()
-        r = dev.search_device(Qt, p, lv.MatrixSource(Et), smem_lut=not gl)
+        r = dev.search_device(Qt, p, lv.MatrixSource(Et), **kw)
         st = dev.last_stats()
-        res["global" if gl else "smem"] = (r["ids"].cpu().numpy(), st)
-    a, b = res["smem"], res["global"]
-    assert (a[0] == b[0]).all()
+        res[name] = (r["ids"].cpu().numpy(), st)
+    for name in res:
+        assert (res[name][0] == res["global"][0]).all(), name
     for k, (_, st) in res.items():
         gbs = st["adc_bytes"] / (st["frontier_ms"] / 1e3) / 1e9
         out[f"ef{ef}_{k}"] = dict(ms=round(st["frontier_ms"], 3), algorithmic_GBps=round(gbs, 1),
