@@ -46,7 +46,7 @@ CONFIGS = {
     "c1": dict(workload="config-1: 10k passages x 128 tokens, 4-layer d=256 random-init encoder, "
                         "degree-32 pruned graph, PQ m=32, 100 queries top-3",
                n=10_000, seq=128, encoder="c1-4l-d256", pq_m=32, k=3, n_queries=100,
-               batch=100, corpus="uniform"),
+               batch=100, corpus="uniform", cpu_all_queries=True),
     "c2": dict(workload="config-2: 1M passages x 256 tokens (LDA-style topic mixtures), "
                         "BERT-base (768-d) random-init encoder, high-degree-preserving pruned "
                         "graph (M=32, m=6, beta=2%), PQ m=64, 4096-query pool, top-3",
@@ -96,7 +96,9 @@ def load_traffic():
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
     the step's kernels, from the committed ncu launch-list summary
     (profiles/traffic.json, written by tools/summarize_launches.py --json)."""
-    p = ROOT / "profiles" / "traffic.json"
+    p = ROOT / "profiles" / "traffic_r02.json"
+    if not p.exists():
+        p = ROOT / "profiles" / "traffic.json"
     try:
         d = json.loads(p.read_text())
         return {k: {"bytes_per_launch": v["dram_bytes_per_launch"], "source": d.get("source"),
@@ -727,20 +729,25 @@ def batch_sweep(W, cfg, args, dev_index, params, source, hub_cache):
     return out
 
 
-def _cpu_mode(args):
-    """(processes, queries per step): default one complete query per step on
-    all host threads (bounded wall time: ~30 s at config-2); --cpu-procs P runs
-    P single-threaded searches per step in P forked processes (the throughput
-    configuration, minutes per step at config-2)."""
-    procs = args.cpu_procs if args.cpu_procs > 0 else 1
-    return procs, procs
+def _cpu_mode(args, cfg):
+    """(processes, queries per step). Config-2..4 default: one complete query per
+    step on all host threads (bounded wall time: ~20 s at config-2). Config-1
+    default and --cpu-procs P: P single-threaded searches per step in P forked
+    processes (the throughput configuration; minutes per step at config-2)."""
+    if args.cpu_procs > 0:
+        return args.cpu_procs, args.cpu_procs
+    if cfg.get("cpu_all_queries"):
+        return cpu_threads(), cpu_threads()
+    return 1, 1
 
 
 def cpu_baseline(W, cfg, args, ef, hub_cache):
     """Our arm's cpu_baseline: complete queries of the reference CPU search on
     the same workload, hub cache and (ef, rerank%)."""
-    procs, per = _cpu_mode(args)
+    procs, per = _cpu_mode(args, cfg)
     cpu_prepare(W, cfg, args, ef, args.alpha, hub_cache)
+    if cfg.get("cpu_all_queries"):   # config-1: every query (BASELINE.md §3)
+        per = cfg["n_queries"]
     qids = list(range(cfg["n_queries"] - per, cfg["n_queries"]))
     secs, res = cpu_run(qids, procs)
     recall = recall_of(np.array([r[1] for r in res]), W["gt"][qids])
@@ -764,7 +771,7 @@ def run_reference(W, cfg, args, ef, batch, dev_index, params, flops_pp, hub_cach
     rerank% as the GPU arm); value = queries / wall s (see _cpu_mode)."""
     import torch
     from oracle.encoder_ref import make_ref_encoder
-    procs, per = _cpu_mode(args)
+    procs, per = _cpu_mode(args, cfg)
     cores = cpu_threads()
     cpu_prepare(W, cfg, args, ef, args.alpha, hub_cache)
     nq = cfg["n_queries"]
