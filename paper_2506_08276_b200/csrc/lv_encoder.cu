@@ -17,6 +17,7 @@
 // Both are batch-invariant: a passage's embedding never depends on the batch
 // it rides in (the test_vectors.py:145-152 contract).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <type_traits>
@@ -888,12 +889,23 @@ int forward_fused(lv_encoder *e, int64_t ns, int S, int M, float *out, cudaStrea
   return LV_OK;
 }
 
+// tokens per encoder chunk (activations of one chunk live at once); LV_CHUNK_TOKENS
+// overrides the default 2^19 for measurements
+int64_t chunk_tokens(const lv_encoder *) {
+  static const int64_t v = [] {
+    const char *s = std::getenv("LV_CHUNK_TOKENS");
+    const long long x = s ? std::atoll(s) : 0;
+    return x > 0 ? (int64_t)x : ((int64_t)1 << 19);
+  }();
+  return v;
+}
+
 template <typename T>
 int forward(lv_encoder *e, const void *tokens, int token_bytes, int S, const int32_t *d_ids,
             int64_t n_seqs, float *out, cudaStream_t s) {
   const auto &c = e->cfg;
   const int d = c.hidden, ff = c.ffn, H = c.heads, dh = c.hidden / c.heads;
-  const int64_t max_tokens = std::max<int64_t>(S, (int64_t)1 << 19);
+  const int64_t max_tokens = std::max<int64_t>(S, chunk_tokens(e));
   const int64_t chunk = std::max<int64_t>(1, max_tokens / S);
   LV_TRY(ensure_ws(e, std::min<int64_t>(n_seqs, chunk) * S));
   T *x = (T *)e->x, *qkv = (T *)e->qkv, *ctx = (T *)e->ctx, *y = (T *)e->y, *h = (T *)e->h;
