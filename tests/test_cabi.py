@@ -131,3 +131,34 @@ def test_recall_at_k_reference_semantics():
     assert mean_recall([[1, 2], [5, 6]], [[1, 2], [6, 7]]) == 0.75
     with pytest.raises(InvalidArgumentError):
         recall_at_k([1], [])
+
+
+def test_index_create_rejects_rows_beyond_max_degree_and_bad_ids():
+    """lv_index_create validates every CSR row before touching the device
+    (frontier scratch is sized from max_degree; bitmaps are indexed by id)."""
+    import ctypes as C
+    import numpy as np
+    from paper_2506_08276_b200 import _lib
+
+    def create(offsets, nbrs, max_degree):
+        offs = np.asarray(offsets, dtype=np.uint64)
+        nb = np.asarray(nbrs, dtype=np.uint32)
+        d = _lib.IndexDesc()
+        d.n, d.dim, d.metric, d.max_degree, d.level_count = len(offs) - 1, 4, 2, max_degree, 1
+        d.entry_point = 0
+        op = (C.c_void_p * 1)(offs.ctypes.data)
+        npp = (C.c_void_p * 1)(nb.ctypes.data)
+        nnz = (C.c_uint64 * 1)(nb.shape[0])
+        d.level_offsets = C.cast(op, C.POINTER(C.c_void_p))
+        d.level_neighbors = C.cast(npp, C.POINTER(C.c_void_p))
+        d.level_nnz = C.cast(nnz, C.POINTER(C.c_uint64))
+        h = C.c_void_p()
+        rc = _lib.lib().lv_index_create(C.byref(d), 0, C.byref(h))
+        return rc, _lib.lib().lv_last_error().decode()
+
+    rc, msg = create([0, 3, 3, 3], [1, 2, 1], max_degree=2)     # row 0 has 3 > M = 2
+    assert rc == 3 and "exceeds M" in msg
+    rc, msg = create([0, 1, 2, 2], [1, 7], max_degree=2)        # neighbour id 7 >= n = 3
+    assert rc == 3 and "out of range" in msg
+    rc, msg = create([0, 2, 1, 2], [1, 2], max_degree=2)        # offsets not monotone
+    assert rc == 3

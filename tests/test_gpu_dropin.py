@@ -145,3 +145,31 @@ def test_overlay_graph_equals_its_frozen_csr(fx):
                         fx["codes"], qn=fx["qn"])
     _same(a, b)
     assert a[0].results[0][0] != plain[0].results[0][0]
+
+
+def test_failed_search_leaves_no_stale_visited_bits(fx):
+    """A provider failure aborts lv_search_batch mid-traversal with queries in
+    flight; the next search on the same handle must clear their visited sets
+    (workspace dirty flag) and return the reference results."""
+    lv = fx["lv"]
+    from paper_2506_08276_b200.errors import SearchError
+    p = lv.SearchParams(k=3, ef=32, rerank_percent=30.0)
+    ref = lv.search_batch(fx["g"], fx["Q"], p, lv.MatrixSource(fx["E"]), "cosine", fx["model"],
+                          fx["codes"], qn=fx["qn"])
+    bad = lv.ProviderSource(HostProvider(fx["E"], fail_after=2), lambda i: str(i).encode())
+    with pytest.raises(SearchError):
+        lv.search_batch(fx["g"], fx["Q"], p, bad, "cosine", fx["model"], fx["codes"], qn=fx["qn"])
+    good = lv.ProviderSource(HostProvider(fx["E"]), lambda i: str(i).encode())
+    _same(ref, lv.search_batch(fx["g"], fx["Q"], p, good, "cosine", fx["model"], fx["codes"],
+                               qn=fx["qn"]))
+
+
+def test_zero_query_rejected_for_cosine_two_level(fx):
+    """adc_build raises for a zero query under cosine (pq.py:163-166)."""
+    lv = fx["lv"]
+    from paper_2506_08276_b200.errors import InvalidArgumentError
+    Q = fx["Q"][:4].copy()
+    Q[2] = 0.0
+    with pytest.raises(InvalidArgumentError):
+        lv.search_batch(fx["g"], Q, lv.SearchParams(k=3, ef=32), lv.MatrixSource(fx["E"]),
+                        "cosine", fx["model"], fx["codes"])
