@@ -577,7 +577,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int blk = 0;
+    // per-row LayerNorm statistics (EPF_LN_IN / EPF_RES_LN) of a tile, loaded one
+    // tile ahead so their global-load latency hides behind the current tile
+    // (both boxes of a tile share rows)
+    auto row_stats = [&](int t, float4 &st) {
+      st = make_float4(0.f, 1.f, 0.f, 1.f);
+      if (t >= num_tiles) return;
+      const int row = (t / n_tiles) * 256 + (int)rank * 128 + q * 32 + lane;
+      if (row >= M) return;
+      if (fl & EPF_LN_IN) {
+        const float2 v = __ldg(ep.ln_in + row);
+        st.x = v.x;
+        st.y = v.y;
+      }
+      if (fl & EPF_RES_LN) {
+        const float2 v = __ldg(ep.res_ln + row);
+        st.z = v.x;
+        st.w = v.y;
+      }
+    };
+    float4 st_cur, st_next;
+    row_stats(pair, st_cur);
     for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+      row_stats(tile + n_pairs, st_next);
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
 #pragma unroll 1
@@ -594,17 +616,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         box_coords(tile, b, x, y);
         const int grow = y + lane;  // this thread's output row
         const bool live = grow < M;
-        float mu_i = 0.f, rs_i = 1.f, mu_r = 0.f, rs_r = 1.f;
-        if ((fl & EPF_LN_IN) && live) {
-          const float2 t = __ldg(ep.ln_in + grow);
-          mu_i = t.x;
-          rs_i = t.y;
-        }
-        if ((fl & EPF_RES_LN) && live) {
-          const float2 t = __ldg(ep.res_ln + grow);
-          mu_r = t.x;
-          rs_r = t.y;
-        }
+        const float mu_i = st_cur.x, rs_i = st_cur.y, mu_r = st_cur.z, rs_r = st_cur.w;
         {  // next box's column vectors into the other buffer
           const int nt = b == 0 ? tile : tile + n_pairs;
           if (nt < num_tiles) {
@@ -771,6 +783,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      st_cur = st_next;
     }
     if (lane == 0) bulk_wait<0>();
   }
