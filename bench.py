@@ -703,12 +703,28 @@ def main():
 
 def batch_sweep(W, cfg, args, dev_index, params, source, hub_cache):
     """Config-5-style sweep: one timed step (query encoding + recompute search,
-    CUDA events) per concurrent-query count B, at the tuned (ef, rerank%).
-    Workspaces for B are sized first by a dry recompute search (untimed)."""
+    CUDA events) per concurrent-query count B. The rerank% is the tuned one;
+    ef is re-tuned on each B-query set (tune_ef, resident-matrix mode) so every
+    point meets the recall target on its own queries. Workspaces for B are
+    sized first by a dry recompute search (untimed)."""
     import torch
     import paper_2506_08276_b200 as lv
+    from paper_2506_08276_b200.evaluation import tune_ef
     out = []
     for B in args.sweep:
+        Qs, gts = W["Q"][:B].contiguous(), W["gt"][:B]
+        memo = {}
+
+        def rec(ef):
+            if ef not in memo:
+                r = dev_index.search_device(Qs, lv.SearchParams(k=params.k, ef=ef,
+                                                                rerank_percent=params.rerank_percent),
+                                            lv.MatrixSource(W["E"]))
+                memo[ef] = recall_of(r["ids"][:B].cpu().numpy(), gts)
+            return memo[ef]
+
+        tr = tune_ef(rec, params.k, args.ef_max, args.recall)
+        params = lv.SearchParams(k=params.k, ef=tr.ef, rerank_percent=params.rerank_percent)
         qt = W["qtok_dev"][:B].contiguous()
         dev_index.search_device(W["Q"][:B].contiguous(), params, lv.ProviderSource(W["prov"]),
                                 cache=hub_cache, dry_matrix=W["E"], max_inflight=B)
@@ -721,10 +737,11 @@ def batch_sweep(W, cfg, args, dev_index, params, source, hub_cache):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         st = dev_index.last_stats()
-        rec = recall_of(res["ids"][:B].cpu().numpy(), W["gt"][:B])
+        rec_b = recall_of(res["ids"][:B].cpu().numpy(), gts)
         out.append({"concurrent_queries": B, "queries_per_s": round(B / (ms / 1e3), 2),
+                    "ef": tr.ef, "rerank_percent": params.rerank_percent,
                     "physical_per_query": round(st["physical_encodes"] / B, 1),
-                    "recall_at_3": round(rec, 4), "ms": round(ms, 1)})
+                    "recall_at_3": round(rec_b, 4), "ms": round(ms, 1)})
         log(f"sweep: B={B} {out[-1]}")
     return out
 
