@@ -176,6 +176,10 @@ class LeannSearcher:
         vecs = np.ascontiguousarray(vectors, dtype=np.float32).reshape(ids.shape[0], -1)
         if vecs.shape[1] != self._pending_vecs.shape[1]:
             raise InvalidArgumentError("pending vectors do not match the index dim")
+        if ids.size and (ids.min() < self.graph.n or
+                         np.intersect1d(ids, self._pending_ids).size or
+                         np.unique(ids).size != ids.size):
+            raise InvalidArgumentError("pending ids must be new (>= n) and distinct")
         self._pending_ids = np.concatenate([self._pending_ids, ids])
         self._pending_vecs = np.concatenate([self._pending_vecs, vecs])
         self._pending_dev = None
