@@ -69,3 +69,36 @@ def test_engine_search_reaches_the_device_path(engine, monkeypatch):
     monkeypatch.setattr(slimvec.index, "run_search", run_search)
     with pytest.raises(DeviceError):
         engine.search(np.ones(32, np.float32), SearchParams(k=3, ef=16))
+
+
+def test_reference_engine_opens_a_directory_written_here(tmp_path, monkeypatch):
+    """index.build's directory layout (graph/pq/deleted/items/meta/mutations) is
+    opened by the reference's own Engine.open (index.py:235-274): meta keys,
+    provider hash, loaders and the item store all accept it. The GPU encoder
+    registers as an external-kind provider, whose reference client requires an
+    endpoint (SLIMVEC_ENDPOINT) before the caller swaps in EncoderProvider."""
+    monkeypatch.setenv("SLIMVEC_ENDPOINT", "unix:/tmp/lv-encoder.sock")
+    import shutil
+    from conftest import GOLDEN
+    from slimvec.index import Engine, read_meta as ref_read_meta
+    from paper_2506_08276_b200.builder import GpuBuildParams
+    from paper_2506_08276_b200.encoder import TokenStore
+    from paper_2506_08276_b200.graph import load_graph, save_deleted
+    from paper_2506_08276_b200.index import meta_for, read_meta, write_meta
+    src = GOLDEN / "small_cos"
+    g = load_graph(src / "graph.bin")
+    d = tmp_path / "ix"
+    d.mkdir()
+    shutil.copy(src / "graph.bin", d / "graph.bin")
+    shutil.copy(src / "pq.bin", d / "pq.bin")
+    save_deleted(g.deleted, d / "deleted.bin")
+    TokenStore(np.arange(g.n * 4, dtype=np.uint16).reshape(g.n, 4)).save(d)
+    dim = int(np.load(src / "matrix.npy").shape[1])
+    write_meta(d / "meta.txt", meta_for(GpuBuildParams(max_degree=g.max_degree), g.n, dim))
+    (d / "mutations.log").write_bytes(b"")
+    assert ref_read_meta(d / "meta.txt") == read_meta(d / "meta.txt")
+    eng = Engine.open(d)
+    try:
+        assert eng.dim == dim and eng.mutable.overlay.n == g.n and eng.metric == "cosine"
+    finally:
+        eng.close()
