@@ -185,3 +185,41 @@ def test_streaming_adc_bit_exact_vs_oracle(lv, m):
     got = dev.adc_score(table, ids)
     ref = approx_distance_many(table, codes[ids])
     assert np.array_equal(got.view(np.uint32), np.asarray(ref, dtype=np.float32).view(np.uint32))
+
+
+def test_empty_batch_returns_nothing(lv):
+    d = GOLDEN / "small_cos"
+    g = lv.load_graph(d / "graph.bin")
+    model, codes = lv.load_pq(d / "pq.bin")
+    E = np.load(d / "matrix.npy")
+    reps = lv.search_batch(g, np.zeros((0, E.shape[1]), np.float32), lv.SearchParams(k=3, ef=8),
+                           lv.MatrixSource(E), "cosine", model, codes)
+    assert reps == []
+
+
+def test_ef_n_full_rerank_equals_brute_force(lv):
+    """ef = n, rerank 100% reduces to exhaustive search (reference
+    test_search.py:196-205): the results are the reference-order brute force."""
+    from paper_2506_08276_b200.evaluation import ground_truth
+    d = GOLDEN / "small_cos"
+    g = lv.load_graph(d / "graph.bin")
+    model, codes = lv.load_pq(d / "pq.bin")
+    E, Q = np.load(d / "matrix.npy"), np.load(d / "queries.npy")
+    reps = lv.search_batch(g, Q, lv.SearchParams(k=5, ef=g.n, rerank_percent=100.0),
+                           lv.MatrixSource(E), "cosine", model, codes)
+    gt = ground_truth(E, Q, 5, "cosine")
+    assert [[i for i, _ in r.results] for r in reps] == gt
+
+
+def test_all_deleted_returns_no_results_but_traverses(lv):
+    """Deleted nodes stay traversable and are filtered only at k_best
+    (search.py:324,426): with every node deleted the result list is empty."""
+    d = GOLDEN / "small_cos"
+    g = lv.load_graph(d / "graph.bin")
+    model, codes = lv.load_pq(d / "pq.bin")
+    E, Q = np.load(d / "matrix.npy"), np.load(d / "queries.npy")
+    g.deleted = np.ones(g.n, dtype=bool)
+    reps = lv.search_batch(g, Q[:8], lv.SearchParams(k=3, ef=16), lv.MatrixSource(E), "cosine",
+                           model, codes)
+    assert all(r.results == [] and r.recomputations > 0 for r in reps)
+    g.deleted = np.zeros(g.n, dtype=bool)
