@@ -255,9 +255,12 @@ def tune(W, cfg, args, dev_index, hub_cache=None):
                                     cache=hub_cache, dry_matrix=W["E"])
             t["physical_per_query"] = dev_index.last_stats()["physical_encodes"] / batch
             log(f"tune: alpha={t['alpha']} ef={t['ef']} physical/q={t['physical_per_query']:.1f}")
-        best = min(ok, key=lambda t: (t["physical_per_query"], -t["recall"]))
+        key = lambda t: (t["physical_per_query"], -t["recall"])  # noqa: E731
     else:
-        best = min(ok, key=lambda t: (t["recomputes"], -t["recall"]))
+        key = lambda t: (t["recomputes"], -t["recall"])  # noqa: E731
+    if not any(t["feasible"] for t in table):   # nothing reaches the target: best recall
+        key = lambda t: (-t["recall"],)  # noqa: E731
+    best = min(ok, key=key)
     return best, table
 
 
@@ -411,6 +414,8 @@ def main():
                     help="CPU reference: P single-threaded searches per step in P forked "
                          "processes (default: one query per step on all host threads)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--alpha-sweep", action="store_true",
+                    help="also time one step per tuned rerank percent (config-4 sweep)")
     ap.add_argument("--batch-sweep", default="",
                     help="also time one step at each of these concurrent-query counts "
                          "(config-5 style), e.g. 256,1024,4096,16384")
@@ -696,9 +701,41 @@ def main():
     }
     if args.sweep and world == 1:
         line["batch_sweep"] = batch_sweep(W, cfg, args, dev_index, params, source, hub_cache)
+    if args.alpha_sweep and world == 1:
+        line["rerank_sweep"] = rerank_sweep(W, cfg, args, dev_index, table, source, hub_cache,
+                                            batch)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(W, cfg, args, ef, hub_cache)
     print(json.dumps(line), flush=True)
+
+
+def rerank_sweep(W, cfg, args, dev_index, table, source, hub_cache, batch):
+    """Recompute-ratio sweep (config-4: rerank 5-30%): one timed step per
+    rerank percent of the tuning table at its tuned ef (the minimal ef reaching
+    the target, or --ef-max when none does), with the step's recall."""
+    import torch
+    import paper_2506_08276_b200 as lv
+    out = []
+    for t in table:
+        p = lv.SearchParams(k=cfg["k"], ef=t["ef"], rerank_percent=t["alpha"])
+        qt = W["qtok_dev"][:batch].contiguous()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        Qb = W["enc"].encode(qt)
+        res = dev_index.search_device(Qb, p, source, cache=hub_cache, max_inflight=args.inflight)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        st = dev_index.last_stats()
+        out.append({"rerank_percent": t["alpha"], "ef": t["ef"], "feasible": t["feasible"],
+                    "queries_per_s": round(batch / (ms / 1e3), 2),
+                    "recall": round(recall_of(res["ids"][:batch].cpu().numpy(),
+                                              W["gt"][:batch]), 4),
+                    "physical_per_query": round(st["physical_encodes"] / batch, 1),
+                    "logical_per_query": round(float(res["counters"][:batch, 0].double()
+                                                     .mean().item()), 1)})
+        log(f"rerank sweep: {out[-1]}")
+    return out
 
 
 def batch_sweep(W, cfg, args, dev_index, params, source, hub_cache):
