@@ -43,7 +43,7 @@
  *                        <- the encoder's attention (BERT-style MHA; config-4 causal GQA),
  *                           exported for unit tests of the tcgen05 attention kernels
  *   lv_encoder_set_fused_ln, lv_encoder_set_split_residual, lv_set_gemm_mode,
- *   lv_set_attention_mode
+ *   lv_set_attention_mode, lv_set_fused_qkv_attention
  *                        <- kernel-variant switches for parity tests and A/B measurements
  *
  * Conventions: plain pointers and sizes only. Unless LV_IO_DEVICE is set in a
@@ -177,6 +177,10 @@ typedef struct {
   double attn_ms;
   double attn_flops;      /* 4*S^2*dh*H per sequence */
   double attn_bytes;      /* qkv read + context written */
+  int64_t fused_launches; /* timed fused QKV-projection + attention launches (S = 256, dh = 64) */
+  double fused_ms;
+  double fused_flops;     /* 2*M*3d*d (projection) + 4*S^2*dh*H per sequence (attention) */
+  double fused_bytes;     /* x read + W_qkv + context written */
 } lv_encoder_stats_t;
 
 typedef struct {
@@ -293,6 +297,11 @@ int lv_set_gemm_mode(int mode);
  * 2 = tcgen05 kernel with every third softmax exponential by polynomial on the FMA pipe
  * (experiment), any other value = tcgen05 kernel where it applies. Returns the previous mode. */
 int lv_set_attention_mode(int mode);
+/* 1 (default): the bf16 BERT encoder at S = 256, dh = 64 runs the QKV projection
+ * and the attention of a layer as one SM-pair kernel (qkv never written to HBM);
+ * 0: the unfused pair GEMM + attn_tc_kernel (bit-identical results). Returns the
+ * previous setting. */
+int lv_set_fused_qkv_attention(int enable);
 
 #ifdef __cplusplus
 }

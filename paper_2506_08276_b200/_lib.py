@@ -75,7 +75,8 @@ class EncoderStats(C.Structure):
         ("passages", C.c_int64), ("gemm_launches", C.c_int64),
         ("gemm_ms", C.c_double), ("gemm_flops", C.c_double), ("gemm_bytes", C.c_double),
         ("attn_launches", C.c_int64), ("attn_ms", C.c_double), ("attn_flops", C.c_double),
-        ("attn_bytes", C.c_double),
+        ("attn_bytes", C.c_double), ("fused_launches", C.c_int64), ("fused_ms", C.c_double),
+        ("fused_flops", C.c_double), ("fused_bytes", C.c_double),
     ]
 
 
@@ -118,6 +119,7 @@ EXPORTS = {
     "lv_encoder_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "lv_set_gemm_mode": (C.c_int, [C.c_int]),
     "lv_set_attention_mode": (C.c_int, [C.c_int]),
+    "lv_set_fused_qkv_attention": (C.c_int, [C.c_int]),
     "lv_attention_gqa_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "lv_encoder_set_fused_ln": (C.c_int, [C.c_void_p, C.c_int]),

@@ -357,9 +357,16 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
       }
       const float mc = mx * scale_log2;
       // pass 2: p = 2^(s*c - max*c), row sum, P (bf16) over the consumed columns
-      float sum = 0.f;
+      // the row sum is kept as two halves (columns [0, S/2) and [S/2, S)) added at
+      // the end: the order the fused QKV + attention kernel (lv_qkv_attn.cu), whose
+      // two warps per row each own one half, reproduces bit for bit
+      float sum_a = 0.f, sum = 0.f;
 #pragma unroll 1
       for (int c = 0; c < S / 32; ++c) {
+        if (c == S / 64) {
+          sum_a = sum;
+          sum = 0.f;
+        }
         uint32_t r0[32];
         tmem_ld32(tb + 32 * c, r0);
         uint32_t w[16];
@@ -374,6 +381,7 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
         }
         tmem_st16(tb + 16 * c, w);
       }
+      sum = sum_a + sum;
       tmem_st_wait();
       fence_before();
       __syncwarp();

@@ -614,11 +614,13 @@ struct lv_encoder {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used;
   std::vector<double> ev_flops, ev_bytes;  // algorithmic work of each timed launch
-  std::vector<int> ev_kind;                // 0 GEMM, 1 attention
+  std::vector<int> ev_kind;                // 0 GEMM, 1 attention, 2 fused QKV + attention
   double gemm_bytes = 0.0;
   int64_t attn_launches = 0;
   double attn_ms = 0.0, attn_flops = 0.0, attn_bytes = 0.0;
   double gemm_ms = 0.0, gemm_flops = 0.0;
+  int64_t fused_launches = 0;
+  double fused_ms = 0.0, fused_flops = 0.0, fused_bytes = 0.0;
   int64_t gemm_launches = 0;
   int64_t passages = 0;
   ~lv_encoder() {
@@ -820,6 +822,32 @@ int timed_attention(lv_encoder *e, const __nv_bfloat16 *qkv, __nv_bfloat16 *ctx,
   return LV_OK;
 }
 
+// fused QKV projection + attention (S = 256, dh = 64) with optional CUDA-event
+// timing: algorithmic work = the projection's 2*M*3d*d plus attention's
+// 4*S^2*dh*H FLOPs per sequence; bytes = x + W_qkv read, context written
+int fused_qkv_attention(lv_encoder *e, const __nv_bfloat16 *x, const void *w_qkv,
+                        const EpiParams &q, __nv_bfloat16 *ctx, int ns, int S, int H, int dh,
+                        cudaStream_t s) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (e->profile) {
+    e0 = take_event(e);
+    e1 = take_event(e);
+    cudaEventRecord(e0, s);
+  }
+  const int d = H * dh;
+  LV_TRY(qkv_attention_fused(x, (const __nv_bfloat16 *)w_qkv, q.bias, q.colc,
+                             (q.flags & EPF_LN_IN) ? q.ln_in : nullptr, ctx, ns, S, H, dh, d, s));
+  if (e->profile) {
+    cudaEventRecord(e1, s);
+    e->ev_used.emplace_back(e0, e1);
+    const double M = (double)ns * S;
+    e->ev_flops.push_back(2.0 * M * 3.0 * d * d + 4.0 * ns * (double)S * S * dh * H);
+    e->ev_bytes.push_back(2.0 * (M * d + 3.0 * d * (double)d + M * d));
+    e->ev_kind.push_back(2);
+  }
+  return LV_OK;
+}
+
 int finalize_stats(lv_encoder *e, float2 *dst, int M, cudaStream_t s) {
   ln_stats_finalize_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(
       e->st_part, e->cfg.hidden / 64, dst, M);
@@ -844,12 +872,16 @@ int forward_fused(lv_encoder *e, int64_t ns, int S, int M, float *out, cudaStrea
       q.colc = L.c_qkv;
       q.ln_in = e->st2;
       q.flags = EPF_LN_IN;
-      LV_TRY(fused_gemm(e, x, L.w_qkv_f, nullptr, qkv, M, 3 * d, d, q, s));
     } else {
       q.bias = L.b_qkv;
-      LV_TRY(fused_gemm(e, x, L.w_qkv, nullptr, qkv, M, 3 * d, d, q, s));
     }
-    LV_TRY(timed_attention(e, qkv, ctx, (int)ns, S, H, dh, s));
+    const void *w_qkv = P ? L.w_qkv_f : L.w_qkv;
+    if (g_fuse_qkv_attn && S == 256 && dh == 64) {  // qkv stays on chip (lv_qkv_attn.cu)
+      LV_TRY(fused_qkv_attention(e, x, w_qkv, q, ctx, (int)ns, S, H, dh, s));
+    } else {
+      LV_TRY(fused_gemm(e, x, w_qkv, nullptr, qkv, M, 3 * d, d, q, s));
+      LV_TRY(timed_attention(e, qkv, ctx, (int)ns, S, H, dh, s));
+    }
     EpiParams o;
     o.bias = L.b_o;
     o.flags = EPF_RES | EPF_STATS | (split ? EPF_SPLIT : 0);
@@ -1080,6 +1112,11 @@ void encoder_collect_profile(lv_encoder *enc) {
         enc->gemm_flops += enc->ev_flops[i];
         enc->gemm_bytes += enc->ev_bytes[i];
         enc->gemm_launches += 1;
+      } else if (enc->ev_kind[i] == 2) {
+        enc->fused_ms += ms;
+        enc->fused_flops += enc->ev_flops[i];
+        enc->fused_bytes += enc->ev_bytes[i];
+        enc->fused_launches += 1;
       } else {
         enc->attn_ms += ms;
         enc->attn_flops += enc->ev_flops[i];
@@ -1389,6 +1426,12 @@ int lv_encoder_set_fused_ln(lv_encoder *enc, int enable) {
   return LV_OK;
 }
 
+int lv_set_fused_qkv_attention(int enable) {
+  const int prev = g_fuse_qkv_attn;
+  g_fuse_qkv_attn = enable != 0;
+  return prev;
+}
+
 int lv_set_attention_mode(int mode) {
   const int prev = g_attn_mode;
   g_attn_mode = mode;
@@ -1415,6 +1458,10 @@ int lv_encoder_stats(lv_encoder *enc, lv_encoder_stats_t *st) {
   st->attn_ms = enc->attn_ms;
   st->attn_flops = enc->attn_flops;
   st->attn_bytes = enc->attn_bytes;
+  st->fused_launches = enc->fused_launches;
+  st->fused_ms = enc->fused_ms;
+  st->fused_flops = enc->fused_flops;
+  st->fused_bytes = enc->fused_bytes;
   return LV_OK;
 }
 
@@ -1430,6 +1477,8 @@ int lv_encoder_reset_stats(lv_encoder *enc) {
   enc->gemm_bytes = 0.0;
   enc->attn_launches = 0;
   enc->attn_ms = enc->attn_flops = enc->attn_bytes = 0.0;
+  enc->fused_launches = 0;
+  enc->fused_ms = enc->fused_flops = enc->fused_bytes = 0.0;
   return LV_OK;
 }
 

@@ -120,6 +120,14 @@ cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
 cudaError_t attention_gqa_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int S,
                                int Hq, int Hkv, int dh, bool causal, cudaStream_t s);
 extern int g_attn_mode;  // see lv_set_attention_mode (leann_b200.h)
+// Fused QKV projection + attention of a post-LN BERT layer on an SM pair
+// (lv_qkv_attn.cu): ctx = attention(epi(x . W_qkv^T)) with the QKV epilogue of
+// tc_gemm_ex (bias; LN-in when ln_in != null: rstd (acc - mean colc) + bias);
+// S = 256, dh = 64, K % 64 == 0. Bit-identical to tc_gemm_ex + attention_bf16.
+int qkv_attention_fused(const __nv_bfloat16 *x, const __nv_bfloat16 *w_qkv, const float *bias,
+                        const float *colc, const float2 *ln_in, __nv_bfloat16 *ctx, int n_seqs,
+                        int S, int H, int dh, int K, cudaStream_t s);
+extern int g_fuse_qkv_attn;  // see lv_set_fused_qkv_attention (leann_b200.h)
 cudaError_t attention_f32(const float *qkv, float *out, int n_seqs, int S, int H, int dh,
                           cudaStream_t s);
 
