@@ -233,8 +233,7 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
   using namespace tc;
   using C = atc::Cfg<S>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still shared space
   // Q|K and V of a stage have separate full/empty barriers: Q and K are free
   // once the item's last Q.K^T MMA completes, so the next item's Q|K load
   // starts a softmax earlier than a per-stage release would allow
@@ -735,8 +734,7 @@ __global__ void __launch_bounds__(atq::kThreads, 1)
                           int n_seqs, int S, int Hq, int Hkv) {
   using namespace tc;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still shared space
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 2 * atq::kGroupBytes);
   // per group r: [0] q_full [1] q_free [2,3] ring_full [4,5] ring_free [6] s_full
   // [7] s_free [8] p_full [9] pv_done [10] o_full [11] o_free

@@ -69,8 +69,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    int epi) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still shared space
   uint8_t *sA = smem;
   uint8_t *sB = smem + C::kStages * C::kABytes;
   uint64_t *full = reinterpret_cast<uint64_t *>(sB + C::kStages * C::kBBytes);
@@ -299,8 +298,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const EpiParams ep) {
   constexpr int BN = 256;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still shared space
   uint8_t *sA = smem;
   constexpr bool kRes = PairCfg<kMode>::kRes;
   constexpr bool kSplit = PairCfg<kMode>::kSplit;

@@ -25,14 +25,19 @@
 //  3. S = Q.K^T (pair MMA, M = 256, N = 256 keys, K = 64) -> TMEM [256, 512):
 //     the B operand's N split across the pair IS the key split, so no K exchange.
 //  4. Softmax: the two warps sharing a TMEM lane quarter own columns [0, 128) and
-//     [128, 256) of a row (max / sum exchanged through shared memory); P (bf16)
-//     written over the consumed scores (tcgen05.st).
+//     [128, 256) of a row (max / sum exchanged through shared memory); each writes
+//     its P (bf16) over its own consumed scores (tcgen05.st).
 //  5. O = P.V (pair TS-MMA: P from each CTA's TMEM, V MN-major, M = 256, N = 64)
-//     -> TMEM [192, 256); ctx = O / rowsum, 64 bytes per thread and row.
+//     -> TMEM [192, 256); ctx = O / rowsum through a swizzled shared-memory tile and
+//     one TMA store per 32 rows (full 128-byte lines).
 // Pipelining (one MMA thread, cycle k): G(k), PV(k-2), S(k-1); epilogue cycle k:
-// drain(k), O-epilogue(k-2), softmax(k-1) — the GEMM of item k runs on the tensor
-// pipe while the epilogue warps do the softmax of item k-1. Q/K are double
-// buffered, V triple buffered (P.V of item k-2 is issued after G(k)).
+// drain(k), O-epilogue(k-2), softmax(k-1) — the GEMM of item k+1 runs on the
+// tensor pipe while the epilogue warps do the softmax of item k. Q and K are
+// single-buffered (drain(k) writes them once S(k-1) completed), V double-buffered
+// (once P.V(k-2) completed), which leaves 4 operand stages in shared memory.
+// Cross-CTA traffic is asynchronous only: the peer's V half goes as one 8 KB
+// shared::cluster bulk copy completing on the receiver's mbarrier (no generic
+// remote stores, so no cluster-scope memory fences on the critical path).
 //
 // Numerics: every value equals the unfused path bit for bit — the same fp32
 // accumulators (fixed K order), the same epilogue expression, the same
@@ -41,6 +46,7 @@
 #include <cuda.h>
 
 #include <cfloat>
+#include <cstdio>
 
 #include "lv_kernels.cuh"
 #include "lv_tc.cuh"
@@ -52,20 +58,27 @@ using namespace tc;
 namespace qa {
 constexpr int kThreads = 64 + 8 * 32;
 constexpr int kS = 256, kDh = 64;
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr int kABytes = 128 * 64 * 2;   // A half per stage (128 rows x 64 K)
 constexpr int kBBytes = 96 * 64 * 2;    // B half per stage (96 weight rows x 64 K)
 constexpr int kQKBytes = 128 * 128;     // [128][64] bf16
 constexpr int kVBytes = kS * 64;        // [256 keys][32 dims] bf16
+constexpr int kStgBytes = 128 * 64;     // this CTA's keys x the peer's 32 dims
 constexpr int kOffB = kStages * kABytes;
 constexpr int kOffQ = kOffB + kStages * kBBytes;
-constexpr int kOffK = kOffQ + 2 * kQKBytes;
-constexpr int kOffV = kOffK + 2 * kQKBytes;
-constexpr int kOffRed = kOffV + 3 * kVBytes;    // float [2][2][128]: row max / sum halves
-constexpr int kOffBar = kOffRed + 2 * 2 * 128 * 4;
+constexpr int kOffK = kOffQ + kQKBytes;
+constexpr int kOffV = kOffK + kQKBytes;
+constexpr int kOffStg = kOffV + 2 * kVBytes;
+constexpr int kOffCtx = kOffStg + kStgBytes;     // [128 rows][64] bf16 context tile, 128B swizzle
+constexpr int kOffCol = kOffCtx + kQKBytes;      // float [2 items][bias 192 | colc 192]
+constexpr int kOffRed = kOffCol + 2 * 384 * 4;   // float [128 rows][max h0, max h1, sum h0, sum h1]
+constexpr int kOffBar = kOffRed + 128 * 16;
 constexpr int kSmem = kOffBar + 256 + 1024;
 constexpr uint32_t kColAcc = 0, kColO = 192, kColS = 256;
-static_assert(kOffQ % 1024 == 0 && kOffV % 1024 == 0, "swizzled regions need 1 KB alignment");
+constexpr int kBarDrain = 5;  // named barrier of the 8 epilogue warps (ids 1-4: row pairs)
+static_assert(kOffQ % 1024 == 0 && kOffK % 1024 == 0 && kOffV % 1024 == 0 &&
+                  kOffStg % 1024 == 0 && kOffCtx % 1024 == 0,
+              "swizzled regions need 1 KB alignment");
 static_assert(kSmem <= 232448, "shared memory");
 }  // namespace qa
 
@@ -75,18 +88,30 @@ __device__ __forceinline__ float ex2_fast(float x) {
   return y;
 }
 
+// shared::cta -> shared::cluster bulk copy (async proxy), completion (complete_tx)
+// on an mbarrier of the destination CTA
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst, const void *src, uint32_t bytes,
+                                                  uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "r"(smem_u32(src)), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
     qkv_attn_pair_kernel(const __grid_constant__ CUtensorMap tmA,
-                         const __grid_constant__ CUtensorMap tmB, const float *__restrict__ bias,
+                         const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmC, const float *__restrict__ bias,
                          const float *__restrict__ colc, const float2 *__restrict__ ln_in,
                          __nv_bfloat16 *__restrict__ ctx, int n_items, int H, int K,
                          float scale_log2) {
   using namespace qa;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still shared space
   uint8_t *sA = smem, *sB = smem + kOffB, *sQ = smem + kOffQ, *sK = smem + kOffK,
-          *sV = smem + kOffV;
+          *sV = smem + kOffV, *sStg = smem + kOffStg, *sCtx = smem + kOffCtx;
+  float *sCol = reinterpret_cast<float *>(smem + kOffCol);
   float *red = reinterpret_cast<float *>(smem + kOffRed);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + kOffBar);
   uint64_t *empty = full + kStages;
@@ -97,7 +122,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
   uint64_t *p_full = s_full + 1;        // [2]
   uint64_t *o_full = p_full + 2;
   uint64_t *o_empty = o_full + 1;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(o_empty + 1);
+  uint64_t *v_in = o_empty + 1;         // [2] the peer's V half landed here (complete_tx)
+  uint64_t *v_fwd = v_in + 2;           // [2] leader: the peer's v_in completed
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(v_fwd + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -109,13 +136,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
     }
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 16);
-    mbar_init(&qkv_ready[0], 16);
-    mbar_init(&qkv_ready[1], 16);
     mbar_init(s_full, 1);
-    mbar_init(&p_full[0], 16);
-    mbar_init(&p_full[1], 16);
     mbar_init(o_full, 1);
     mbar_init(o_empty, 16);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qkv_ready[i], 16);
+      mbar_init(&p_full[i], 16);
+      mbar_init(&v_in[i], 1);
+      mbar_init(&v_fwd[i], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -199,24 +228,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
           mbar_wait(&p_full[j & 1], (uint32_t)(j >> 1) & 1);
           if (j >= 1) mbar_wait(o_empty, (uint32_t)(j - 1) & 1);
           fence_after();
-          const uint32_t vb = smem_u32(sV + (j % 3) * kVBytes);
+          const uint32_t vb = smem_u32(sV + (j & 1) * kVBytes);
 #pragma unroll
-          for (int t = 0; t < kS / 16; ++t)  // 16 keys = 1024 bytes of V per K step
-            umma_ts_pair(tmem + kColO, tmem + kColS + 8 * t, sw64_desc(vb + 1024 * t), idesc_o,
-                         t != 0);
+          for (int t = 0; t < kS / 16; ++t)  // 16 keys = 1024 bytes of V per K step; P of
+            // keys [128, 256) sits at S-region columns [128, 192) (softmax, below)
+            umma_ts_pair(tmem + kColO, tmem + kColS + 8 * t + (t >= 8 ? 64 : 0),
+                         sw64_desc(vb + 1024 * t), idesc_o, t != 0);
           umma_commit_pair(o_full);
         }
         if (k >= 1 && k - 1 < n) {  // S(k-1) = Q.K^T over the sequence's 256 keys
           const int j = k - 1;
-          mbar_wait_acq_cluster(&qkv_ready[j & 1], (uint32_t)(j >> 1) & 1);
+          const uint32_t ph = (uint32_t)(j >> 1) & 1;
+          mbar_wait(&qkv_ready[j & 1], ph);  // Q, K, own V halves written (both CTAs)
+          mbar_wait(&v_in[j & 1], ph);       // the peer's V half landed in the leader
+          mbar_wait(&v_fwd[j & 1], ph);      // ... and the leader's half in the peer
           fence_after();
-          const uint64_t a0 = sw128_desc(smem_u32(sQ + (j & 1) * kQKBytes));
-          const uint64_t b0 = sw128_desc(smem_u32(sK + (j & 1) * kQKBytes));
+          const uint64_t a0 = sw128_desc(smem_u32(sQ));
+          const uint64_t b0 = sw128_desc(smem_u32(sK));
 #pragma unroll
           for (int t = 0; t < kDh / 16; ++t)
             umma_bf16_pair(tmem + kColS, a0 + 2 * t, b0 + 2 * t, idesc_s, t != 0);
           umma_commit_pair(s_full);
         }
+      }
+    } else if (!leader && lane == 0) {  // forward the completion of this CTA's V copies
+      const uint32_t fwd0 = map_to_rank(&v_fwd[0], 0), fwd1 = map_to_rank(&v_fwd[1], 0);
+      for (int j = 0; j < n; ++j) {
+        mbar_wait(&v_in[j & 1], (uint32_t)(j >> 1) & 1);
+        mbar_arrive_remote((j & 1) ? fwd1 : fwd0);
       }
     }
   } else {
@@ -224,18 +263,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
     const int q = warp & 3;     // TMEM lane quarter
     const int half = ew >> 2;   // column half of the row this warp owns
     const int row = q * 32 + lane;  // row of the CTA's 128
+    const int et = ew * 32 + lane;  // epilogue thread 0..255
+    const bool elected = et == 0;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t acc_empty_l = map_to_rank(acc_empty, 0);
     const uint32_t o_empty_l = map_to_rank(o_empty, 0);
     const uint32_t qkv_ready_l0 = map_to_rank(&qkv_ready[0], 0);
     const uint32_t qkv_ready_l1 = map_to_rank(&qkv_ready[1], 0);
     const uint32_t p_full_l0 = map_to_rank(&p_full[0], 0), p_full_l1 = map_to_rank(&p_full[1], 0);
+    const uint32_t peer = rank ^ 1u;
+    const uint32_t peer_vin0 = map_to_rank(&v_in[0], peer), peer_vin1 = map_to_rank(&v_in[1], peer);
+    const uint32_t peer_v0 = map_to_rank(sV + rank * kStgBytes, peer);  // my keys in the peer's V
     const int bar_id = 1 + q;  // the two warps of this lane quarter
+    // column vectors (bias, LN-in colc) of item i -> sCol[i & 1] by cp.async, one item ahead
+    auto load_cols = [&](int i) {
+      if (et < 96) {
+        const int item = pair + i * n_pairs;
+        const int h = item % H;
+        const int v = et / 48, c = et % 48;  // vector, 16-byte chunk of its 192 columns
+        const int col = c * 4;               // 0..188: q [0,64) k [64,128) v [128,192)
+        const int gcol = (col >> 6) * D + h * kDh + (col & 63);
+        const float *src = v ? colc : bias;
+        if (src)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                           smem_u32(sCol + (i & 1) * 384 + v * 192 + col)),
+                       "l"(src + gcol)
+                       : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (n > 0) load_cols(0);
     float sum_prev = 1.f;      // row sum of the item whose softmax ran last
     for (int k = 0; k < n + 2; ++k) {
       if (k < n) {  // drain(k): accumulators -> Q, K, V tiles in shared memory
-        const int item = pair + k * n_pairs;
-        const int seq = item / H, h = item - seq * H;
+        const int seq = (pair + k * n_pairs) / H;
+        const int grow = seq * kS + (int)rank * 128 + row;
+        float mu = 0.f, rs = 1.f;
+        if (ln_in) {
+          const float2 st = __ldg(ln_in + grow);
+          mu = st.x;
+          rs = st.y;
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        named_sync(kBarDrain, 256);  // item k's column vectors visible; buffer (k+1)&1 free
+        if (k + 1 < n) load_cols(k + 1);
         mbar_wait(acc_full, (uint32_t)k & 1);
         fence_after();
         uint32_t r[96];
@@ -252,29 +323,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(acc_empty_l);
-        const int grow = seq * kS + (int)rank * 128 + row;
-        float mu = 0.f, rs = 1.f;
-        if (ln_in) {
-          const float2 st = __ldg(ln_in + grow);
-          mu = st.x;
-          rs = st.y;
-        }
-        const uint32_t sw = (uint32_t)(row & 7);
+        // epilogue of tc_gemm_pair_kernel (EPF_LN_IN or bias only), bf16 packed in place
+        const float *cb = sCol + (k & 1) * 384 + half * 96;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const int n0 = half * 96 + 32 * c;  // accumulator column: q [0,64) k [64,128) v [128,192)
-          const int part = n0 >> 6, dim0 = n0 & 63;
-          const int gcol = part * D + h * kDh + dim0;  // column of the unfused qkv row
-          const float4 *b4 = reinterpret_cast<const float4 *>(bias + gcol);
-          const float4 *c4 = reinterpret_cast<const float4 *>(colc + gcol);
-          uint32_t w[16];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const float4 bb = __ldg(b4 + j);
+            const float4 bb = *reinterpret_cast<const float4 *>(cb + 32 * c + 4 * j);
             const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
             float v[4];
             if (ln_in) {
-              const float4 cc = __ldg(c4 + j);
+              const float4 cc = *reinterpret_cast<const float4 *>(cb + 192 + 32 * c + 4 * j);
               const float cv[4] = {cc.x, cc.y, cc.z, cc.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e)
@@ -283,46 +342,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
 #pragma unroll
               for (int e = 0; e < 4; ++e) v[e] = __uint_as_float(r[32 * c + 4 * j + e]) + bv[e];
             }
-            w[2 * j] = pack_bf16(v[0], v[1]);
-            w[2 * j + 1] = pack_bf16(v[2], v[3]);
+            r[16 * c + 2 * j] = pack_bf16(v[0], v[1]);
+            r[16 * c + 2 * j + 1] = pack_bf16(v[2], v[3]);
           }
+        }
+        // Q / K of item k-1 consumed and its V copies complete (S(k-1) waited for them);
+        // V slot k&1 (item k-2) consumed by P.V(k-2) in both CTAs
+        if (k >= 1) mbar_wait(s_full, (uint32_t)(k - 1) & 1);
+        if (k >= 2) mbar_wait(o_full, (uint32_t)(k - 2) & 1);
+        const uint32_t sw = (uint32_t)(row & 7), kw = (uint32_t)((row >> 1) & 3);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int n0 = half * 96 + 32 * c;  // accumulator column: q [0,64) k [64,128) v [128,192)
+          const int part = n0 >> 6, dim0 = n0 & 63;
+          const uint32_t *w = &r[16 * c];
           if (part < 2) {  // Q or K: K-major [128][64], 128-byte swizzle
-            uint8_t *dst = (part == 0 ? sQ : sK) + (k & 1) * kQKBytes + row * 128;
+            uint8_t *dst = (part == 0 ? sQ : sK) + row * 128;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const uint32_t chunk = (uint32_t)(dim0 >> 3) + j;
               *reinterpret_cast<uint4 *>(dst + ((chunk ^ sw) << 4)) =
                   make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
             }
-          } else {  // V dims [dim0, dim0 + 32) -> CTA dim0 / 32, key row of the sequence
-            const int key = (int)rank * 128 + row;
-            const uint32_t kw = (uint32_t)((key >> 1) & 3);
-            uint8_t *dst = sV + (k % 3) * kVBytes + key * 64;
-            const uint32_t target = (uint32_t)(dim0 >> 5);
-            if (target == rank) {
+          } else {  // V dims [dim0, dim0 + 32) belong to CTA dim0 / 32; key = 128 rank + row
+            uint8_t *dst = (uint32_t)(dim0 >> 5) == rank
+                               ? sV + (k & 1) * kVBytes + ((int)rank * 128 + row) * 64
+                               : sStg + row * 64;  // byte image of the peer's rows
 #pragma unroll
-              for (int j = 0; j < 4; ++j)
-                *reinterpret_cast<uint4 *>(dst + (((uint32_t)j ^ kw) << 4)) =
-                    make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-            } else {
-              const uint32_t rdst = map_to_rank(dst, target);
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                st_cluster_v4(rdst + (((uint32_t)j ^ kw) << 4),
-                              make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]));
-            }
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4 *>(dst + (((uint32_t)j ^ kw) << 4)) =
+                  make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
           }
         }
-        // generic-proxy writes (own and peer shared memory) before the MMA reads them
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          asm volatile("fence.acq_rel.cluster;" ::: "memory");
-          mbar_arrive_release_cluster((k & 1) ? qkv_ready_l1 : qkv_ready_l0);
+        fence_async_smem();            // generic writes -> visible to the async proxy
+        named_sync(kBarDrain, 256);    // the CTA's Q, K, V and staging rows are written
+        if (elected) {
+          mbar_expect_tx(&v_in[k & 1], kStgBytes);  // the peer's 8 KB for item k
+          bulk_copy_to_peer(peer_v0 + (uint32_t)((k & 1) * kVBytes), sStg, kStgBytes,
+                            (k & 1) ? peer_vin1 : peer_vin0);
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote((k & 1) ? qkv_ready_l1 : qkv_ready_l0);
       }
-      if (k >= 2) {  // O-epilogue(k-2): ctx row slice = O / rowsum
+      if (k >= 2) {  // O-epilogue(k-2): ctx = O / rowsum, staged per lane quarter, TMA store
         const int j = k - 2;
         const int item = pair + j * n_pairs;
         const int seq = item / H, h = item - seq * H;
@@ -334,66 +396,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(o_empty_l);
         const float inv = 1.f / sum_prev;
-        const size_t grow = (size_t)seq * kS + rank * 128 + row;
-        uint4 *op = reinterpret_cast<uint4 *>(ctx + grow * D + h * kDh + half * 32);
+        uint32_t w[16];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 u;
-          u.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
-          u.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
-          u.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
-          u.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
-          op[v] = u;
+        for (int e = 0; e < 16; ++e)
+          w[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
+        uint8_t *tile = sCtx + q * 32 * 128;  // this lane quarter's [32 rows][64] box
+        if (half == 0 && lane == 0) bulk_wait_read<0>();  // the previous store has read it
+        named_sync(bar_id, 64);
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          *reinterpret_cast<uint4 *>(tile + lane * 128 + ((uint32_t)((4 * half + v) ^ (lane & 7)) << 4)) =
+              make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+        fence_async_smem();
+        named_sync(bar_id, 64);
+        if (half == 0 && lane == 0) {
+          tma_store_2d(&tmC, tile, h * kDh, seq * kS + (int)rank * 128 + q * 32);
+          bulk_commit();
         }
       }
       if (k >= 1 && k - 1 < n) {  // softmax(k-1) over this warp's 128 score columns
         const int j = k - 1;
         mbar_wait(s_full, (uint32_t)j & 1);
         fence_after();
-        uint32_t s[128];
-        {
-          const uint32_t tb = tmem + lane_off + kColS + (uint32_t)(half * 128);
-          uint32_t(&s0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[0]);
-          uint32_t(&s1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[32]);
-          uint32_t(&s2)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[64]);
-          uint32_t(&s3)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[96]);
-          tmem_ld32_nowait(tb, s0);
-          tmem_ld32_nowait(tb + 32, s1);
-          tmem_ld32_nowait(tb + 64, s2);
-          tmem_ld32_nowait(tb + 96, s3);
-          tmem_ld_wait();
-        }
+        // scores in two passes over TMEM (pass 1: row max, pass 2: exponentials); each
+        // half writes its P over its own consumed score columns: keys [0, 128) at TMEM
+        // columns [0, 64) of the S region, keys [128, 256) at [128, 192)
+        const uint32_t tb = tmem + lane_off + kColS + (uint32_t)(half * 128);
+        float *rr = red + row * 4;  // this row's max / sum halves, shared by the row's two warps
         float mx = -FLT_MAX;
+#pragma unroll 1
+        for (int c = 0; c < 4; c += 2) {
+          uint32_t s0[32], s1[32];
+          tmem_ld32_nowait(tb + 32 * c, s0);
+          tmem_ld32_nowait(tb + 32 * c + 32, s1);
+          tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(s[e]));
-        red[half * 128 + row] = mx;
-        named_sync(bar_id, 64);  // both halves' scores are in registers from here on
-        mx = fmaxf(mx, red[(half ^ 1) * 128 + row]);
+          for (int e = 0; e < 32; ++e)
+            mx = fmaxf(mx, fmaxf(__uint_as_float(s0[e]), __uint_as_float(s1[e])));
+        }
+        rr[half] = mx;
+        named_sync(bar_id, 64);
+        mx = fmaxf(mx, rr[half ^ 1]);
         const float mc = mx * scale_log2;
         float part = 0.f;
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < 4; ++c) {
+          uint32_t s0[32];
+          tmem_ld32(tb + 32 * c, s0);
           uint32_t w[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const float p0 = ex2_fast(fmaf(__uint_as_float(s[32 * c + 2 * e]), scale_log2, -mc));
-            const float p1 =
-                ex2_fast(fmaf(__uint_as_float(s[32 * c + 2 * e + 1]), scale_log2, -mc));
+            const float p0 = ex2_fast(fmaf(__uint_as_float(s0[2 * e]), scale_log2, -mc));
+            const float p1 = ex2_fast(fmaf(__uint_as_float(s0[2 * e + 1]), scale_log2, -mc));
             part += p0 + p1;
             w[e] = pack_bf16(p0, p1);
           }
-          tmem_st16(tmem + lane_off + kColS + (uint32_t)(half * 64 + 16 * c), w);
+          tmem_st16(tb + 16 * c, w);
         }
         tmem_st_wait();
-        red[256 + half * 128 + row] = part;
+        rr[2 + half] = part;
         fence_before();
         named_sync(bar_id, 64);
-        sum_prev = half == 0 ? part + red[256 + 128 + row] : red[256 + row] + part;
+        sum_prev = half == 0 ? part + rr[3] : rr[2] + part;
         __syncwarp();
         if (lane == 0) mbar_arrive_remote((j & 1) ? p_full_l1 : p_full_l0);
       }
     }
   }
+  if (warp >= 2 && lane == 0) bulk_wait<0>();  // context stores complete before exit
   fence_before();
   cluster_sync_all();
   if (warp == 1) {
@@ -419,6 +489,9 @@ int qkv_attention_fused(const __nv_bfloat16 *x, const __nv_bfloat16 *w_qkv, cons
              LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(x) failed");
   LV_REQUIRE(make_tma_2d_bf16(&tb, w_qkv, (uint64_t)K, (uint64_t)3 * D, (uint64_t)K * 2, 64, 32),
              LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(W_qkv) failed");
+  CUtensorMap tc_;
+  LV_REQUIRE(make_tma_2d_bf16(&tc_, ctx, (uint64_t)D, (uint64_t)n_seqs * S, (uint64_t)D * 2, 64, 32),
+             LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(ctx) failed");
   static bool attr = false;
   if (!attr) {
     LV_CHECK_CUDA(cudaFuncSetAttribute(qkv_attn_pair_kernel,
@@ -428,9 +501,18 @@ int qkv_attention_fused(const __nv_bfloat16 *x, const __nv_bfloat16 *w_qkv, cons
   const int items = n_seqs * H;
   const int pairs = std::min(items, tc_gemm_num_sms() / 2);
   qkv_attn_pair_kernel<<<2 * pairs, qa::kThreads, qa::kSmem, s>>>(
-      ta, tb, bias, colc, ln_in, ctx, items, H, K, 1.4426950408889634f / 8.0f);
+      ta, tb, tc_, bias, colc, ln_in, ctx, items, H, K, 1.4426950408889634f / 8.0f);
   note_launch();
-  LV_CHECK_CUDA(cudaGetLastError());
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, qkv_attn_pair_kernel);
+    std::fprintf(stderr, "qkv_attn_pair_kernel launch: %s (regs %d, static smem %zu, max dyn %d, "
+                 "max threads %d, requested smem %d)\n", cudaGetErrorString(err), fa.numRegs,
+                 fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.maxThreadsPerBlock,
+                 qa::kSmem);
+  }
+  LV_CHECK_CUDA(err);
   return LV_OK;
 }
 
