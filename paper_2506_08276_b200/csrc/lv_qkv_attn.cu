@@ -104,8 +104,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
                          const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const float *__restrict__ bias,
                          const float *__restrict__ colc, const float2 *__restrict__ ln_in,
-                         __nv_bfloat16 *__restrict__ ctx, int n_items, int H, int K,
-                         float scale_log2) {
+                         __nv_bfloat16 *__restrict__ ctx, int n_seqs, int H, int K,
+                         int seq_major, float scale_log2) {
   using namespace qa;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still shared space
@@ -159,7 +159,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
   const uint32_t tmem = *tslot;
 
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-  const int n = n_items > pair ? (n_items - pair + n_pairs - 1) / n_pairs : 0;
+  // Work assignment. seq_major (large launches): pair p owns sequences p, p + P, ... and
+  // runs their H heads back to back, so a sequence's x rows come from DRAM once (head 0)
+  // and from L2 for the other heads, and the producer prefetches the next sequence's
+  // rows into L2 one K block per head. Otherwise items (sequence, head) are dealt out
+  // round-robin (small launches: every pair busy).
+  const int n_items = n_seqs * H;
+  const int n = seq_major ? (n_seqs > pair ? (n_seqs - pair + n_pairs - 1) / n_pairs : 0) * H
+                          : (n_items > pair ? (n_items - pair + n_pairs - 1) / n_pairs : 0);
+  auto item_of = [&](int i, int &seq, int &h) {
+    if (seq_major) {
+      const int t = i / H;
+      seq = pair + t * n_pairs;
+      h = i - t * H;
+    } else {
+      const int item = pair + i * n_pairs;
+      seq = item / H;
+      h = item - seq * H;
+    }
+  };
   const int D = H * kDh;
   const int kblocks = K / 64;
 
@@ -173,8 +191,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int i = 0; i < n; ++i) {
-        const int item = pair + i * n_pairs;
-        const int seq = item / H, h = item - seq * H;
+        int seq, h;
+        item_of(i, seq, h);
+        if (seq_major && h < kblocks && seq + n_pairs < n_seqs)  // next sequence's K block h -> L2
+          asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&tmA),
+                       "r"(h * 64), "r"((seq + n_pairs) * kS + (int)rank * 128)
+                       : "memory");
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = map_to_rank(&full[stage], 0);
@@ -278,8 +300,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
     // column vectors (bias, LN-in colc) of item i -> sCol[i & 1] by cp.async, one item ahead
     auto load_cols = [&](int i) {
       if (et < 96) {
-        const int item = pair + i * n_pairs;
-        const int h = item % H;
+        int seq, h;
+        item_of(i, seq, h);
         const int v = et / 48, c = et % 48;  // vector, 16-byte chunk of its 192 columns
         const int col = c * 4;               // 0..188: q [0,64) k [64,128) v [128,192)
         const int gcol = (col >> 6) * D + h * kDh + (col & 63);
@@ -296,7 +318,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
     float sum_prev = 1.f;      // row sum of the item whose softmax ran last
     for (int k = 0; k < n + 2; ++k) {
       if (k < n) {  // drain(k): accumulators -> Q, K, V tiles in shared memory
-        const int seq = (pair + k * n_pairs) / H;
+        int seq, h_unused;
+        item_of(k, seq, h_unused);
         const int grow = seq * kS + (int)rank * 128 + row;
         float mu = 0.f, rs = 1.f;
         if (ln_in) {
@@ -386,8 +409,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(qa::kThreads, 1)
       }
       if (k >= 2) {  // O-epilogue(k-2): ctx = O / rowsum, staged per lane quarter, TMA store
         const int j = k - 2;
-        const int item = pair + j * n_pairs;
-        const int seq = item / H, h = item - seq * H;
+        int seq, h;
+        item_of(j, seq, h);
         mbar_wait(o_full, (uint32_t)j & 1);
         fence_after();
         uint32_t o[32];
@@ -500,8 +523,9 @@ int qkv_attention_fused(const __nv_bfloat16 *x, const __nv_bfloat16 *w_qkv, cons
   }
   const int items = n_seqs * H;
   const int pairs = std::min(items, tc_gemm_num_sms() / 2);
+  const int seq_major = n_seqs >= 8 * pairs;
   qkv_attn_pair_kernel<<<2 * pairs, qa::kThreads, qa::kSmem, s>>>(
-      ta, tb, tc_, bias, colc, ln_in, ctx, items, H, K, 1.4426950408889634f / 8.0f);
+      ta, tb, tc_, bias, colc, ln_in, ctx, n_seqs, H, K, seq_major, 1.4426950408889634f / 8.0f);
   note_launch();
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {

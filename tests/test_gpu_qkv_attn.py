@@ -38,7 +38,7 @@ def _cfg(name):
 
 
 @pytest.mark.parametrize("name,n", [("d256", 1), ("d256", 37), ("bert-2l", 3), ("bert-2l", 29),
-                                    ("bert-base", 13)])
+                                    ("bert-base", 13), ("d256", 600), ("bert-2l", 700)])
 def test_fused_qkv_attention_bit_identical_to_unfused(lv, name, n):
     from paper_2506_08276_b200.encoder import GpuEncoder, init_weights, synthetic_tokens
     cfg = _cfg(name)
@@ -57,10 +57,12 @@ def test_fused_qkv_attention_bit_identical_to_unfused(lv, name, n):
 
 
 def test_fused_qkv_attention_batch_invariant(lv):
+    """Large launches run sequence-major (a pair owns whole sequences), small ones deal
+    (sequence, head) items round-robin: the split below mixes both."""
     from paper_2506_08276_b200.encoder import GpuEncoder, init_weights, synthetic_tokens
     cfg = _cfg("bert-2l")
     enc = GpuEncoder(cfg, init_weights(cfg, seed=5), precision="bf16")
-    tok = synthetic_tokens(75, 256, cfg.vocab, seed=6)
+    tok = synthetic_tokens(700, 256, cfg.vocab, seed=6)
     whole = _encode(enc, tok, True)
     parts = np.concatenate([_encode(enc, tok[:1], True), _encode(enc, tok[1:40], True),
                             _encode(enc, tok[40:], True)])
