@@ -658,6 +658,21 @@ def main():
                 "algorithmic_bytes_per_launch": est["attn_bytes"] / na,
                 "tensor_tflops": round(attn_tf, 1), "launches": est["attn_launches"],
                 "share_of_step": round(est["attn_ms"] / ms, 4) if ms else None})
+    if est.get("fused_ms"):
+        nf = max(1, est["fused_launches"])
+        fused_tf = est["fused_flops"] / (est["fused_ms"] / 1e3) / 1e12
+        rooflines.append({
+            "kernel": ("qkv_attn_pair_kernel (fused QKV projection + attention on an SM pair: "
+                       "tcgen05 GEMM N=192 per head, Q.K^T / P.V pair MMAs, qkv never in HBM)"),
+            "bound": "tensor", "achieved": round(fused_tf, 1), "peak": gemm_peak,
+            "unit": "TFLOP/s", "frac": round(fused_tf / gemm_peak, 4),
+            "traffic": traffic.get("qkv_attn_pair_kernel"),
+            "peak_source": f"{peaks_kind} bf16 sustained",
+            "flops_per_launch": est["fused_flops"] / nf,
+            "algorithmic_bytes_per_launch": est["fused_bytes"] / nf,
+            "hbm_gbs": round(est["fused_bytes"] / (est["fused_ms"] / 1e3) / 1e9, 1),
+            "launches": est["fused_launches"],
+            "share_of_step": round(est["fused_ms"] / ms, 4) if ms else None})
     rooflines.append({
         "kernel": "frontier_kernel (CSR gather + ADC + AQ/EQ + exact scoring)", "bound": "hbm",
         "achieved": round(frontier_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
