@@ -92,6 +92,25 @@ def load_peaks():
     return dict(FALLBACK_PEAKS), "fallback"
 
 
+def fused_l2_feed(est, ecfg, S, clocks):
+    """L2 -> shared-memory operand traffic of qkv_attn_pair_kernel against the chip's L2
+    throughput cap (~6300 B/cycle, /opt/skills/guides/B300_MICROARCH.md "LTS throughput
+    cap"): per (sequence, head) each CTA of the pair TMA-loads its 128 x-rows (128 x d x 2 B)
+    and 96 weight rows (96 x d x 2 B) for every K block."""
+    d, H = ecfg.hidden, ecfg.heads
+    per_seq_layer = 2.0 * S * 3 * d * d + 4.0 * S * S * d
+    items = est["fused_flops"] / per_seq_layer * H
+    per_item = 2 * (128 + 96) * d * 2
+    mhz = (clocks or {}).get("sm_mhz") or 0
+    if not est["fused_ms"] or not mhz:
+        return None
+    bpc = items * per_item / (est["fused_ms"] / 1e3) / (mhz * 1e6)
+    return {"bytes_per_item": per_item, "items": int(round(items)),
+            "achieved_bytes_per_cycle": round(bpc, 1), "cap_bytes_per_cycle": 6300,
+            "frac_of_cap": round(bpc / 6300, 3), "sm_mhz": mhz,
+            "note": "L2 throughput cap measured on B300 (guide); tensor frac is bounded by it"}
+
+
 def load_traffic():
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
     the step's kernels, from the committed ncu launch-list summary
@@ -671,6 +690,7 @@ def main():
             "flops_per_launch": est["fused_flops"] / nf,
             "algorithmic_bytes_per_launch": est["fused_bytes"] / nf,
             "hbm_gbs": round(est["fused_bytes"] / (est["fused_ms"] / 1e3) / 1e9, 1),
+            "l2_feed": fused_l2_feed(est, W["ecfg"], cfg["seq"], clocks),
             "launches": est["fused_launches"],
             "share_of_step": round(est["fused_ms"] / ms, 4) if ms else None})
     rooflines.append({
