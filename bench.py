@@ -111,6 +111,19 @@ def fused_l2_feed(est, ecfg, S, clocks):
             "note": "L2 throughput cap measured on B300 (guide); tensor frac is bounded by it"}
 
 
+def gemm_l2_feed(est, clocks):
+    """L2 -> shared-memory operand traffic of tc_gemm_pair_kernel: per 256 x 256 tile and
+    64-deep K block each CTA of the pair loads a 128 x 64 A half and a 128 x 64 B half
+    (2 x 16 KB), i.e. 64 KB per 2*256*256*64 FLOP = 1/128 byte per FLOP, against the chip's
+    L2 throughput cap (~6300 B/cycle, B300_MICROARCH.md)."""
+    mhz = (clocks or {}).get("sm_mhz") or 0
+    if not est["gemm_ms"] or not mhz:
+        return None
+    bpc = est["gemm_flops"] / 128.0 / (est["gemm_ms"] / 1e3) / (mhz * 1e6)
+    return {"bytes_per_flop": 1 / 128, "achieved_bytes_per_cycle": round(bpc, 1),
+            "cap_bytes_per_cycle": 6300, "frac_of_cap": round(bpc / 6300, 3), "sm_mhz": mhz}
+
+
 def load_traffic():
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
     the step's kernels, from the committed ncu launch-list summary
@@ -653,6 +666,7 @@ def main():
                 "peak_source": f"{peaks_kind} bf16 sustained",
                 "launches": est["gemm_launches"], "flops_per_launch": est["gemm_flops"] / nl,
                 "algorithmic_bytes_per_launch": est["gemm_bytes"] / nl,
+                "l2_feed": gemm_l2_feed(est, clocks),
                 "share_of_step": round(est["gemm_ms"] / ms, 4) if ms else None}
     rooflines = [roofline]
     if est["attn_ms"]:
