@@ -285,17 +285,15 @@ int lv_attention_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int
 int lv_attention_gqa_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S, int32_t Hq,
                           int32_t Hkv, int32_t dh, int32_t causal, void *stream);
 /* GEMM kernel selection: 0 = auto (2-CTA cta_group::2 kernel when N % 256 == 0),
- * 1 = 1-CTA kernel only; + 2 = 3-buffer/3-stage epilogue for short-K residual GEMMs
- * (experiment; measured slower than the default 2-buffer/4-stage kernel); + 4 = the
+ * 1 = 1-CTA kernel only; + 4 = the
  * 2-buffer/4-stage kernel also for long-K (K > 1024) residual GEMMs instead of the
  * default 1-buffer/5-stage one; + 8 = the 1-buffer/5-stage split-residual kernel also
  * for short-K split-residual GEMMs (default: 2-buffer/3-stage).
  * Returns the previous mode. */
 int lv_set_gemm_mode(int mode);
 /* Attention kernel selection: 0 = auto (tcgen05/TMEM kernel for dh == 64 and
- * S in {128, 256}, else the mma.sync kernel), 1 = mma.sync kernel only,
- * 2 = tcgen05 kernel with every third softmax exponential by polynomial on the FMA pipe
- * (experiment), any other value = tcgen05 kernel where it applies. Returns the previous mode. */
+ * S in {128, 256}, else the mma.sync kernel), 1 = mma.sync kernel only, any other value =
+ * tcgen05 kernel where it applies. Returns the previous mode. */
 int lv_set_attention_mode(int mode);
 /* 1 (default): the bf16 BERT encoder at S = 256, dh = 64 runs the QKV projection
  * and the attention of a layer as one SM-pair kernel (qkv never written to HBM);

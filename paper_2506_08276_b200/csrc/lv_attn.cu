@@ -212,21 +212,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// 2^x for x <= 0 on the FMA/ALU pipes (attention mode 2 evaluates every
-// third exponential this way to offload the MUFU pipe): x = j + f, j = rint(x)
-// by magic-number rounding, 2^f from a degree-3 least-squares polynomial on
-// [-0.5, 0.5] (max relative error 1.8e-4, below the 2^-9 half-ulp of the
-// bf16 P it feeds), j added to the exponent field.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -125.f);
-  const float t = x + 12582912.f;  // 1.5 * 2^23
-  const float j = t - 12582912.f;
-  const float f = x - j;
-  const float p = fmaf(fmaf(fmaf(0.05460262f, f, 0.24192413f), f, 0.69331648f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
-template <int S, int kPoly>
+template <int S>
 __global__ void __launch_bounds__(atc::kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out,
                    int n_items, int H, float scale_log2) {
@@ -373,8 +359,8 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
         for (int e = 0; e < 16; ++e) {
           const float x0 = fmaf(__uint_as_float(r0[2 * e]), scale_log2, -mc);
           const float x1 = fmaf(__uint_as_float(r0[2 * e + 1]), scale_log2, -mc);
-          const float p0 = (kPoly && (2 * e) % 3 == 2) ? ex2_poly(x0) : ex2_approx(x0);
-          const float p1 = (kPoly && (2 * e + 1) % 3 == 2) ? ex2_poly(x1) : ex2_approx(x1);
+          const float p0 = ex2_approx(x0);
+          const float p1 = ex2_approx(x1);
           sum += p0 + p1;
           w[e] = pack_bf16(p0, p1);
         }
@@ -429,7 +415,7 @@ __global__ void __launch_bounds__(atc::kThreads, 1)
   }
 }
 
-template <int S, int kPoly>
+template <int S>
 cudaError_t launch_attn_tc(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_seqs, int H,
                            cudaStream_t s) {
   using C = atc::Cfg<S>;
@@ -439,14 +425,14 @@ cudaError_t launch_attn_tc(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<S, kPoly>,
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<S>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int items = n_seqs * H;
   const int grid = std::min(items, tc_gemm_num_sms());
-  attn_tc_kernel<S, kPoly><<<grid, atc::kThreads, C::kSmem, s>>>(tm, out, items, H,
+  attn_tc_kernel<S><<<grid, atc::kThreads, C::kSmem, s>>>(tm, out, items, H,
                                                                  1.4426950408889634f / 8.0f);
   note_launch();
   return cudaGetLastError();
@@ -674,11 +660,8 @@ cudaError_t attention_bf16(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
   if (S % 64 != 0 || dh % 16 != 0) return cudaErrorInvalidValue;
   if (g_attn_mode != 1 && dh == 64 && (S == 128 || S == 256)) {
     if (((uintptr_t)qkv & 15) != 0 || ((uintptr_t)out & 15) != 0) return cudaErrorInvalidValue;
-    if (g_attn_mode == 2)  // experiment: every third exponential by polynomial
-      return S == 256 ? launch_attn_tc<256, 1>(qkv, out, n_seqs, H, s)
-                      : launch_attn_tc<128, 1>(qkv, out, n_seqs, H, s);
-    return S == 256 ? launch_attn_tc<256, 0>(qkv, out, n_seqs, H, s)
-                    : launch_attn_tc<128, 0>(qkv, out, n_seqs, H, s);
+    return S == 256 ? launch_attn_tc<256>(qkv, out, n_seqs, H, s)
+                    : launch_attn_tc<128>(qkv, out, n_seqs, H, s);
   }
   const size_t smem = (size_t)3 * S * (dh + 8) * 2;
   const int threads = std::min(256, std::max(32, (S / 16) * 32));

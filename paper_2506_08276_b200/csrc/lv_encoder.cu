@@ -1400,10 +1400,8 @@ int lv_attention_gqa_bf16(const void *qkv, void *out, int32_t n_seqs, int32_t S,
 }
 
 int lv_set_gemm_mode(int mode) {
-  const int prev = g_gemm_mode | (g_short_k != 0 ? 2 : 0) | (g_long_k_single ? 0 : 4) |
-                   (g_split_single ? 8 : 0);
+  const int prev = g_gemm_mode | (g_long_k_single ? 0 : 4) | (g_split_single ? 8 : 0);
   g_gemm_mode = mode & 1;
-  g_short_k = (mode & 2) ? 1024 : 0;
   g_long_k_single = (mode & 4) ? 0 : 1;
   g_split_single = (mode & 8) ? 1 : 0;
   return prev;

@@ -27,7 +27,6 @@
 #include "lv_tc.cuh"
 
 namespace lv {
-int g_short_k = 0;  // residual GEMMs with K <= this use the 3-buffer epilogue (off: measured slower)
 int g_long_k_single = 1;  // residual GEMMs with K > 1024: single box buffer, 5 stages (kMode 4)
 int g_split_single = 0;   // split-residual GEMMs with K <= 1024: kMode 5 instead of 6
 namespace {
@@ -263,10 +262,9 @@ constexpr int kLoBoxBytes = 32 * 64;  // EPF_SPLIT: int8 [32 rows][64 cols], 64-
 // per epilogue warp, two boxes' column vectors (bias, colc, gamma, beta: 64 fp32 each)
 constexpr int kColVecBytes = 4 * 64 * 4;
 constexpr int kColVecTotal = kEpiWarps * 2 * kColVecBytes;
-// kMode 0: no residual (1 box buffer, 5 stages); 1: residual, 2 box buffers,
-// 4 stages (long-K GEMMs); 2: residual, 3 box buffers, 3 stages (short-K
-// GEMMs, whose epilogue is the critical path: the residual load for box b+1
-// need not wait for the store of box b-1 to drain)
+// kMode 0: no residual (1 box buffer, 5 stages); 1: residual, 2 box buffers
+// (the next box's residual prefetched), 4 stages. (A 3-buffer / 3-stage short-K
+// variant measured slower and was removed.)
 template <int kMode>
 struct PairCfg {
   // kMode 3: SwiGLU epilogue (no residual; gate/up interleaved per 64 columns)
@@ -276,12 +274,11 @@ struct PairCfg {
   //          pair per warp, 5 stages
   // kMode 6: split residual, short K: two box pairs (next box's residual
   //          prefetched), 3 stages
-  static constexpr bool kRes = kMode == 1 || kMode == 2 || kMode == 4 || kMode >= 5;
+  static constexpr bool kRes = kMode == 1 || kMode == 4 || kMode >= 5;
   static constexpr bool kSplit = kMode >= 5;
   static constexpr int kStages = (kMode == 0 || kMode == 3 || kMode == 4 || kMode == 5) ? 5
                                  : kMode == 1 ? 4 : 3;
-  static constexpr int kBufs = (kMode == 0 || kMode == 3 || kMode == 4 || kMode == 5) ? 1
-                               : (kMode == 1 || kMode == 6) ? 2 : 3;
+  static constexpr int kBufs = (kMode == 0 || kMode == 3 || kMode == 4 || kMode == 5) ? 1 : 2;
   static constexpr int kPairBytes = kBoxBytes + (kSplit ? kLoBoxBytes : 0);
   static constexpr int kStagingBytes = kEpiWarps * kBufs * kPairBytes;
   static constexpr int kSmem = kStages * kStageBytes2 + kStagingBytes + kColVecTotal + 1024 + 512;
@@ -824,9 +821,6 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<1>::kSmem));
-    LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<2>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       PairCfg<2>::kSmem));
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<3>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<3>::kSmem));
@@ -840,7 +834,6 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
   const int mode = (ep.flags & EPF_SWIGLU) ? 3
                    : !(ep.flags & EPF_RES) ? 0
                    : split ? ((K > 1024 || g_split_single) ? 5 : 6)
-                   : K <= g_short_k ? 2
                    : (K > 1024 && g_long_k_single) ? 4 : 1;
   if (mode == 6)
     tc_gemm_pair_kernel<6><<<2 * pairs, kThreads, PairCfg<6>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
@@ -853,9 +846,6 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
                                                                           M, N, K, ep);
   else if (mode == 3)
     tc_gemm_pair_kernel<3><<<2 * pairs, kThreads, PairCfg<3>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
-                                                                          M, N, K, ep);
-  else if (mode == 2)
-    tc_gemm_pair_kernel<2><<<2 * pairs, kThreads, PairCfg<2>::kSmem, s>>>(ta, tb, to, tr, trl, tol,
                                                                           M, N, K, ep);
   else if (mode == 1)
     tc_gemm_pair_kernel<1><<<2 * pairs, kThreads, PairCfg<1>::kSmem, s>>>(ta, tb, to, tr, trl, tol,

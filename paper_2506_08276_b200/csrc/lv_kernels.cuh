@@ -102,7 +102,6 @@ bool make_tma_2d_u8(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t row
 bool make_tma_2d_bf16(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows,
                       uint64_t row_stride_bytes, int box_cols, int box_rows);
 extern int g_gemm_mode;  // 0 auto (2-CTA pair kernel when N % 256 == 0), 1 force 1-CTA
-extern int g_short_k;    // residual pair GEMMs with K <= g_short_k: 3-buffer epilogue
 extern int g_long_k_single;  // residual pair GEMMs with K > 1024: 1-buffer / 5-stage kernel
 extern int g_split_single;   // split-residual pair GEMMs with K <= 1024: kMode 5 (1 buffer)
 

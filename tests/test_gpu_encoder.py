@@ -148,13 +148,12 @@ def test_encoder_device_tokens_and_provider(lv):
     assert np.array_equal(prov.embed_batch(reqs), host[[3, 7]])
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("n,S,H,dh", [(3, 64, 4, 64), (5, 256, 12, 64), (2, 128, 8, 128),
                                       (2, 512, 16, 64), (7, 128, 4, 64), (61, 256, 12, 64),
                                       (300, 128, 4, 64)])
 def test_attention_bf16_matches_torch(lv, n, S, H, dh, mode):
-    """mode 0: tcgen05/TMEM kernel where it applies (dh 64, S 128/256); 1: mma.sync;
-    2: tcgen05 with every third exponential by polynomial (experiment)."""
+    """mode 0: tcgen05/TMEM kernel where it applies (dh 64, S 128/256); 1: mma.sync."""
     torch = _torch()
     from paper_2506_08276_b200 import _lib
     g = torch.Generator(device="cuda").manual_seed(n * 31 + S)
