@@ -92,36 +92,38 @@ def load_peaks():
     return dict(FALLBACK_PEAKS), "fallback"
 
 
-def fused_l2_feed(est, ecfg, S, clocks):
-    """L2 -> shared-memory operand traffic of qkv_attn_pair_kernel against the chip's L2
-    throughput cap (~6300 B/cycle, /opt/skills/guides/B300_MICROARCH.md "LTS throughput
-    cap"): per (sequence, head) each CTA of the pair TMA-loads its 128 x-rows (128 x d x 2 B)
-    and 96 weight rows (96 x d x 2 B) for every K block."""
+# Observed L2 -> SM operand-feed ceiling of the encoder kernels: ncu
+# l1tex__m_xbar2l1tex_read_bytes over gpu__time_duration of one layer at the bench chunk
+# size gives 9.5 (FFN1), 9.6 (fused QKV + attention) and 9.9 (FFN2) TB/s, independent of the
+# SM clock (1.24-1.57 GHz) — the chip L2 throughput cap (~6300 B per L2 cycle in
+# B300_MICROARCH.md). profiles/r02_l2feed.csv.
+L2_FEED_CAP_TBS = 9.9
+
+
+def l2_feed(bytes_total, ms):
+    if not ms:
+        return None
+    tbs = bytes_total / (ms / 1e3) / 1e12
+    return {"bytes": bytes_total, "achieved_TBps": round(tbs, 2), "cap_TBps": L2_FEED_CAP_TBS,
+            "frac_of_cap": round(tbs / L2_FEED_CAP_TBS, 3),
+            "cap_source": "max L2->SM feed measured by ncu on these kernels (profiles/r02_l2feed.csv)"}
+
+
+def fused_l2_feed(est, ecfg, S):
+    """L2 -> shared-memory operand traffic of qkv_attn_pair_kernel: per (sequence, head)
+    each CTA of the pair TMA-loads its 128 x-rows and 96 weight rows for every K block,
+    2 x (128 + 96) x d x 2 bytes per item."""
     d, H = ecfg.hidden, ecfg.heads
     per_seq_layer = 2.0 * S * 3 * d * d + 4.0 * S * S * d
     items = est["fused_flops"] / per_seq_layer * H
-    per_item = 2 * (128 + 96) * d * 2
-    mhz = (clocks or {}).get("sm_mhz") or 0
-    if not est["fused_ms"] or not mhz:
-        return None
-    bpc = items * per_item / (est["fused_ms"] / 1e3) / (mhz * 1e6)
-    return {"bytes_per_item": per_item, "items": int(round(items)),
-            "achieved_bytes_per_cycle": round(bpc, 1), "cap_bytes_per_cycle": 6300,
-            "frac_of_cap": round(bpc / 6300, 3), "sm_mhz": mhz,
-            "note": "L2 throughput cap measured on B300 (guide); tensor frac is bounded by it"}
+    return l2_feed(items * 2 * (128 + 96) * d * 2, est["fused_ms"])
 
 
-def gemm_l2_feed(est, clocks):
+def gemm_l2_feed(est):
     """L2 -> shared-memory operand traffic of tc_gemm_pair_kernel: per 256 x 256 tile and
     64-deep K block each CTA of the pair loads a 128 x 64 A half and a 128 x 64 B half
-    (2 x 16 KB), i.e. 64 KB per 2*256*256*64 FLOP = 1/128 byte per FLOP, against the chip's
-    L2 throughput cap (~6300 B/cycle, B300_MICROARCH.md)."""
-    mhz = (clocks or {}).get("sm_mhz") or 0
-    if not est["gemm_ms"] or not mhz:
-        return None
-    bpc = est["gemm_flops"] / 128.0 / (est["gemm_ms"] / 1e3) / (mhz * 1e6)
-    return {"bytes_per_flop": 1 / 128, "achieved_bytes_per_cycle": round(bpc, 1),
-            "cap_bytes_per_cycle": 6300, "frac_of_cap": round(bpc / 6300, 3), "sm_mhz": mhz}
+    (2 x 16 KB): 64 KB per 2*256*256*64 FLOP = 1/128 byte per FLOP."""
+    return l2_feed(est["gemm_flops"] / 128.0, est["gemm_ms"])
 
 
 def load_traffic():
@@ -666,7 +668,7 @@ def main():
                 "peak_source": f"{peaks_kind} bf16 sustained",
                 "launches": est["gemm_launches"], "flops_per_launch": est["gemm_flops"] / nl,
                 "algorithmic_bytes_per_launch": est["gemm_bytes"] / nl,
-                "l2_feed": gemm_l2_feed(est, clocks),
+                "l2_feed": gemm_l2_feed(est),
                 "share_of_step": round(est["gemm_ms"] / ms, 4) if ms else None}
     rooflines = [roofline]
     if est["attn_ms"]:
@@ -704,7 +706,7 @@ def main():
             "flops_per_launch": est["fused_flops"] / nf,
             "algorithmic_bytes_per_launch": est["fused_bytes"] / nf,
             "hbm_gbs": round(est["fused_bytes"] / (est["fused_ms"] / 1e3) / 1e9, 1),
-            "l2_feed": fused_l2_feed(est, W["ecfg"], cfg["seq"], clocks),
+            "l2_feed": fused_l2_feed(est, W["ecfg"], cfg["seq"]),
             "launches": est["fused_launches"],
             "share_of_step": round(est["fused_ms"] / ms, 4) if ms else None})
     rooflines.append({
