@@ -182,9 +182,40 @@ __device__ __forceinline__ float adc_one_shared(const float *lut, const uint8_t 
   return __double2float_rn(pairwise_sum(get, m));
 }
 
+// pairwise_block over LUT entries of 8-aligned code runs: the 8 code bytes of
+// each strided step arrive in one 8-byte load (the byte-per-load form spends
+// one dependent LDG per subspace). Same values, same order as pairwise_block.
+__device__ __forceinline__ double adc_block8(const float *__restrict__ lut,
+                                             const uint8_t *__restrict__ code, int lo, int n) {
+  auto lut8 = [&](int base, uint2 c, double (&v)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t w = k < 4 ? c.x : c.y;
+      v[k] = (double)__ldg(lut + (base + k) * 256 + ((w >> (8 * (k & 3))) & 0xffu));
+    }
+  };
+  double r[8];
+  lut8(lo, __ldg(reinterpret_cast<const uint2 *>(code + lo)), r);
+#pragma unroll 4
+  for (int i = 8; i < n; i += 8) {
+    double v[8];
+    lut8(lo + i, __ldg(reinterpret_cast<const uint2 *>(code + lo + i)), v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], v[k]);
+  }
+  return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                   __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+}
+
 // approx distance of one code row against one LUT (pq.py:186-189).
 __device__ __forceinline__ float adc_one(const float *__restrict__ lut,
                                          const uint8_t *__restrict__ code, int m) {
+  if ((m & 7) == 0 && m >= 8 && m <= 256 && (reinterpret_cast<uintptr_t>(code) & 7) == 0) {
+    if (m <= 128) return __double2float_rn(adc_block8(lut, code, 0, m));
+    const int half = (m / 2) - ((m / 2) % 8);
+    return __double2float_rn(__dadd_rn(adc_block8(lut, code, 0, half),
+                                       adc_block8(lut, code, half, m - half)));
+  }
   auto get = [&](int s) -> double {
     return (double)__ldg(lut + s * 256 + __ldg(code + s));
   };
