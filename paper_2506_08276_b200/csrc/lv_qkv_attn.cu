@@ -20,8 +20,8 @@
 //     tc_gemm_pair_kernel, EPF_LN_IN, same expression), bf16 round, then
 //        Q -> own smem [128][64] (K-major, 128B swizzle)   A of S = Q.K^T
 //        K -> own smem [128][64] (K-major, 128B swizzle)   B half of S (keys of CTA r)
-//        V -> [256 keys][32 dims] MN-major 64B-swizzled halves: dims [0, 32) to
-//             CTA 0, [32, 64) to CTA 1 (st.shared::cluster into the peer)  B of P.V
+//        V -> [256 keys][32 dims] MN-major 64B-swizzled halves: dims [0, 32) live in
+//             CTA 0, [32, 64) in CTA 1 (the peer's half: one bulk copy)   B of P.V
 //  3. S = Q.K^T (pair MMA, M = 256, N = 256 keys, K = 64) -> TMEM [256, 512):
 //     the B operand's N split across the pair IS the key split, so no K exchange.
 //  4. Softmax: the two warps sharing a TMEM lane quarter own columns [0, 128) and
@@ -32,7 +32,7 @@
 //     one TMA store per 32 rows (full 128-byte lines).
 // Pipelining (one MMA thread, cycle k): G(k), PV(k-2), S(k-1); epilogue cycle k:
 // drain(k), O-epilogue(k-2), softmax(k-1) — the GEMM of item k+1 runs on the
-// tensor pipe while the epilogue warps do the softmax of item k. Q and K are
+// tensor pipe while the epilogue warps do the softmax of item k-1. Q and K are
 // single-buffered (drain(k) writes them once S(k-1) completed), V double-buffered
 // (once P.V(k-2) completed), which leaves 4 operand stages in shared memory.
 // Cross-CTA traffic is asynchronous only: the peer's V half goes as one 8 KB
