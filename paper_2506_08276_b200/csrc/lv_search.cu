@@ -451,10 +451,21 @@ __device__ void adc_insert(const SearchCtx &c, const SlotPtrs &P, SlotState &S,
   __syncwarp();
   const int L = S.aq_len;
   int carry = F;  // shift of the element just above the current chunk
-  for (int cbase = (L > 0) ? ((L - 1) & ~31) : -1; cbase >= 0; cbase -= 32) {
+  // the AQ chunks are read two ahead: a chunk's writes land at or above its own
+  // positions, so the lower chunks still hold their original keys when prefetched
+  auto ld = [&](int cb) -> unsigned long long {
+    const int i = cb + lane;
+    return (cb >= 0 && i < L) ? P.aq[i] : ~0ull;
+  };
+  int cbase = (L > 0) ? ((L - 1) & ~31) : -1;
+  unsigned long long k0 = ld(cbase), k1 = ld(cbase - 32);
+  for (; cbase >= 0; cbase -= 32) {
+    const unsigned long long k2 = ld(cbase - 64);
     int i = cbase + lane;
     bool act = i < L;
-    unsigned long long key = act ? P.aq[i] : ~0ull;
+    unsigned long long key = k0;
+    k0 = k1;
+    k1 = k2;
     int s = F;
     if (act) {  // number of new keys below `key`
       int lo = 0, hi = F;
