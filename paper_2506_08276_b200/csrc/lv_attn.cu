@@ -423,12 +423,11 @@ cudaError_t launch_attn_tc(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, int n_s
   const uint64_t D3 = (uint64_t)3 * H * 64;
   if (!make_tma_2d_bf16(&tm, qkv, D3, (uint64_t)n_seqs * S, D3 * 2, 64, S))
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;  // per device (first_on_device)
+  if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<S>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int items = n_seqs * H;
   const int grid = std::min(items, tc_gemm_num_sms());
@@ -995,12 +994,11 @@ cudaError_t launch_attn_tc_causal(const __nv_bfloat16 *qkv, __nv_bfloat16 *out, 
   const uint64_t W = (uint64_t)(Hq + 2 * Hkv) * 128;
   if (!make_tma_2d_bf16(&tm, qkv, W, (uint64_t)n_seqs * S, W * 2, 64, 128))
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;  // per device (first_on_device)
+  if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(attn_tc_causal_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, atq::kSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int items = n_seqs * Hq * (S / 128);
   const int grid = std::min(items, tc_gemm_num_sms());

@@ -11,6 +11,17 @@
 namespace lv {
 
 void set_error(const std::string &msg);
+// Kernel attributes (e.g. the dynamic shared-memory opt-in) are per device context:
+// true the first time this is called for the current device with this flag word,
+// which it then marks (launchers keep one word per kernel).
+inline bool first_on_device(unsigned long long &done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done & bit) return false;
+  done |= bit;
+  return true;
+}
 // Process-wide count of kernels this library has launched (lv_kernel_launches).
 void note_launch(long long n = 1);
 

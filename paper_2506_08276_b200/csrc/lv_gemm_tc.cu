@@ -775,11 +775,10 @@ int launch(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const float *bias,
   CUtensorMap ta, tb;
   LV_REQUIRE(make_map(&ta, A, M, K, kBM), LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(A) failed");
   LV_REQUIRE(make_map(&tb, W, N, K, BN), LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(W) failed");
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;  // per device (first_on_device)
+  if (first_on_device(attr_set)) {
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<BN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-    attr_set = true;
   }
   const int tiles = ((M + kBM - 1) / kBM) * (N / BN);
   const int grid = std::min(tiles, tc_gemm_num_sms());
@@ -807,8 +806,8 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
     LV_REQUIRE(make_tma_2d_u8(&tol, ep.out_lo, N, M, (uint64_t)N, 64, 32), LV_ERR_INTERNAL,
                "cuTensorMapEncodeTiled(out lo) failed");
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;  // per device (first_on_device)
+  if (first_on_device(attr_set)) {
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<5>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<5>::kSmem));
@@ -827,7 +826,6 @@ int launch_pair(const __nv_bfloat16 *A, const __nv_bfloat16 *W, const __nv_bfloa
     LV_CHECK_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<4>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<4>::kSmem));
-    attr_set = true;
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = std::min(tiles, tc_gemm_num_sms() / 2);

@@ -515,11 +515,10 @@ int qkv_attention_fused(const __nv_bfloat16 *x, const __nv_bfloat16 *w_qkv, cons
   CUtensorMap tc_;
   LV_REQUIRE(make_tma_2d_bf16(&tc_, ctx, (uint64_t)D, (uint64_t)n_seqs * S, (uint64_t)D * 2, 64, 32),
              LV_ERR_INTERNAL, "cuTensorMapEncodeTiled(ctx) failed");
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;  // per device (first_on_device)
+  if (first_on_device(attr)) {
     LV_CHECK_CUDA(cudaFuncSetAttribute(qkv_attn_pair_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, qa::kSmem));
-    attr = true;
   }
   const int items = n_seqs * H;
   const int pairs = std::min(items, tc_gemm_num_sms() / 2);
