@@ -530,6 +530,14 @@ def main():
         table = []
     else:
         best, table = tune(W, cfg, args, dev_index, hub_cache)
+    if dist is not None:  # every rank runs rank 0's operating point (the timed tuner of
+        # small configs measures wall time, which may differ between ranks)
+        dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
+        choice = torch.tensor([float(best["ef"]), float(best["alpha"])], dtype=torch.float64,
+                              device=dev)
+        dist.broadcast(choice, src=0)
+        if (int(choice[0].item()), float(choice[1].item())) != (best["ef"], best["alpha"]):
+            best = dict(best, ef=int(choice[0].item()), alpha=float(choice[1].item()))
     ef, tuned_recall, feasible = best["ef"], best["recall"], best["feasible"]
     args.alpha = best["alpha"]
     log(f"chosen ef={ef} rerank={args.alpha}% (tuned recall {tuned_recall}, feasible={feasible})")
