@@ -28,6 +28,7 @@ def test_gemm_l2_feed_is_one_byte_per_128_flop():
     # ncu measured 19.41 GB of TMA loads for this launch (profiles/r02_l2feed.csv)
     assert abs(r["bytes"] - 19.41e9) / 19.41e9 < 0.01
     assert abs(r["achieved_TBps"] - 9.49) < 0.02
+    assert b.L2_FEED_CAP_TBS >= 9.9
     assert abs(r["frac_of_cap"] - r["achieved_TBps"] / b.L2_FEED_CAP_TBS) < 2e-3
     assert b.gemm_l2_feed({"gemm_flops": 1.0, "gemm_ms": 0.0}) is None
 
